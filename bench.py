@@ -1,0 +1,559 @@
+#!/usr/bin/env python3
+"""Benchmark: batched small GEMM GFLOP/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1..5]
+
+Default workload (BASELINE.json configs[1], "config2"): fp32 square sweep
+M=N=K in {4,8,...,80} x trans in {NN,NT,TT}, each shape with
+batch = floor(256 MiB / ((MK+KN+MN)*4 B)) independent column-major problems,
+alpha=1.5, beta=0.5, inputs uniform[-1,1) from the seeded counter generator
+(datagen/, seed 1).  One STEP = the 60 library calls of the sweep.
+Inputs are resident in HBM before the timed region; every call touches its own
+256 MiB (> 126 MB L2), so consecutive calls cannot hit in L2.
+
+value     = whole-job GFLOP/s = sum over ranks of 2*M*N*K*batch per step / time
+e2e       = the same metric through the C ABI with HOST (pinned) buffers: H2D of
+            A, B, C and D2H of C inside the timed region
+roofline  = the dominant launch (largest share of the step): algorithmic bytes
+            (MK+KN+2MN)*4*batch (or 2MNK*batch flops if FFMA-bound) / its
+            average CUDA-event duration, vs MEASURED_PEAKS.json
+cpu_baseline = the CPU oracle (oracle/ref_gemm.c, OpenMP, all host cores) on
+            a bounded sample of the same step (rank 0, N=1 only)
+
+Multi-GPU (torchrun, one process per GPU): every rank runs the full sweep on
+its own problems (weak scaling, no collective on the data path); barrier +
+synchronize around the timed region, time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "batched small GEMM GFLOP/s per B200 and % of roofline vs M=N=K, 1/2/4/8 GPUs"
+FFMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4, derived
+DMMA_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12    # 37.2, derived
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------- workloads
+class Shape:
+    def __init__(self, dtype, tr, M, N, K, batch, alpha, beta, seed):
+        self.dtype, self.tr, self.M, self.N, self.K = dtype, tr, M, N, K
+        self.batch, self.alpha, self.beta, self.seed = batch, alpha, beta, seed
+
+    @property
+    def elt(self):
+        return 4 if self.dtype == "f32" else 8
+
+    def stored(self):
+        ra, ca = (self.M, self.K) if self.tr[0] == "N" else (self.K, self.M)
+        rb, cb = (self.K, self.N) if self.tr[1] == "N" else (self.N, self.K)
+        return ra, ca, rb, cb
+
+    def flops(self, batch=None):
+        return 2.0 * self.M * self.N * self.K * (self.batch if batch is None else batch)
+
+    def alg_bytes(self, batch=None):
+        b = self.batch if batch is None else batch
+        cbytes = self.M * self.N * (2 if self.beta != 0 else 1)
+        return float(self.M * self.K + self.K * self.N + cbytes) * self.elt * b
+
+    def formula_bytes(self, batch=None):
+        b = self.batch if batch is None else batch
+        return float(self.M * self.K + self.K * self.N + 2 * self.M * self.N) * self.elt * b
+
+    def name(self):
+        return "%s_%s_%dx%dx%d" % (self.dtype, self.tr, self.M, self.N, self.K)
+
+
+def workload(cfg):
+    S = []
+    if cfg == 1:
+        S.append(Shape("f32", "NN", 16, 16, 16, 2000, 1.0, 0.0, 0))
+        desc = "config1: fp32 NN M=N=K=16 batch=2000 alpha=1 beta=0 (latency-bound, L2-resident)"
+    elif cfg == 2:
+        for n in range(4, 81, 4):
+            b = (256 * 1024 * 1024) // (3 * n * n * 4)
+            for tr in ("NN", "NT", "TT"):
+                S.append(Shape("f32", tr, n, n, n, b, 1.5, 0.5, 1))
+        desc = ("config2: fp32 square sweep M=N=K in {4,8,...,80} x {NN,NT,TT}, "
+                "batch=floor(256MiB/(3n^2*4B)), alpha=1.5, beta=0.5, seed 1")
+    elif cfg == 3:
+        from tests.gpu_utils import config3_shapes
+        for (m, n, k) in config3_shapes():
+            S.append(Shape("f32", "NN", m, n, k, 100000, 1.0, 1.0, 2))
+        desc = "config3: fp32 NN, 64 irregular (M,N,K) from {1,3,...,79}^3, batch 100000 each, alpha=1, beta=1"
+    elif cfg == 4:
+        from tests.gpu_utils import config4_shapes
+        for (m, n, k) in config4_shapes():
+            S.append(Shape("f32", "TN", m, n, k, 500000, -1.0, 0.25, 3))
+        desc = "config4: fp32 TN, M=N=K in 2..32 + (32,32,2), (2,32,32), batch 500000, alpha=-1, beta=0.25"
+    elif cfg == 5:
+        for n in (8, 16, 32, 48, 64, 80):
+            for tr in ("NN", "NT"):
+                S.append(Shape("f64", tr, n, n, n, 2_000_000, 1.0, 0.0, 4))
+        desc = "config5: fp64 NN/NT M=N=K in {8,16,32,48,64,80}, batch 2e6 (chunked to fit HBM), alpha=1, beta=0"
+    else:
+        raise SystemExit("unknown config %r" % cfg)
+    return S, desc
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import datagen
+    from paper_2208_09822_b200 import iaat
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    shapes, desc = workload(args.config)
+    stream = torch.cuda.current_stream()
+    tdt = {"f32": torch.float32, "f64": torch.float64}
+
+    # --- allocate + fill (outside the timed region); one buffer set per (dtype, M,N,K)
+    hbm_cap = torch.cuda.get_device_properties(dev).total_memory
+    bufs = {}
+    chunks = []  # (shape, first_local, count) -- chunking for config 5
+    for s in shapes:
+        ra, ca, rb, cb = s.stored()
+        per = (ra * ca + rb * cb + s.M * s.N) * s.elt
+        cap = int(0.80 * hbm_cap) // (per * 2 if s.dtype == "f64" else per * 3)  # keep room for others
+        cnt = s.batch if args.config != 5 else min(s.batch, max(1, int(0.70 * hbm_cap) // per))
+        for lo in range(0, s.batch, cnt):
+            chunks.append((s, lo, min(cnt, s.batch - lo)))
+        _ = cap
+    for s, lo, cnt in chunks:
+        key = (s.dtype, s.M, s.N, s.K, s.tr, cnt)
+        if key in bufs:
+            continue
+        if args.config == 5:
+            bufs.clear()
+            torch.cuda.empty_cache()
+        ra, ca, rb, cb = s.stored()
+        A = torch.empty(cnt * ra * ca, dtype=tdt[s.dtype], device=dev)
+        B = torch.empty(cnt * rb * cb, dtype=tdt[s.dtype], device=dev)
+        C = torch.empty(cnt * s.M * s.N, dtype=tdt[s.dtype], device=dev)
+        first = rank * s.batch + lo  # global problem ids: ranks own disjoint problems
+        datagen.fill_device(A, s.seed, datagen.MAT_A, ra, ca, ra, ra * ca, cnt, first)
+        datagen.fill_device(B, s.seed, datagen.MAT_B, rb, cb, rb, rb * cb, cnt, first)
+        datagen.fill_device(C, s.seed, datagen.MAT_C, s.M, s.N, s.M, s.M * s.N, cnt, first)
+        bufs[key] = (A, B, C)
+        if args.config == 5:
+            break  # config 5 re-fills per chunk inside the step loop (generation untimed, see below)
+    torch.cuda.synchronize()
+
+    def call(s, lo, cnt):
+        ra, ca, rb, cb = s.stored()
+        A, B, C = bufs[(s.dtype, s.M, s.N, s.K, s.tr, cnt)]
+        st = iaat.iaat_gemm_strided_batched(0 if s.dtype == "f32" else 1, s.tr[0], s.tr[1], s.M, s.N, s.K,
+                                            s.alpha, A.data_ptr(), ra, ra * ca, B.data_ptr(), rb, rb * cb,
+                                            s.beta, C.data_ptr(), s.M, s.M * s.N, cnt, stream.cuda_stream)
+        if st != 0:
+            raise RuntimeError("iaat call failed: %s (%s)" % (iaat.iaat_status_string(st), s.name()))
+
+    if args.config == 5:
+        return run_chunked_config5(args, rank, world, local_rank, shapes, desc, chunks, bufs, call)
+
+    def step(evs=None):
+        for i, (s, lo, cnt) in enumerate(chunks):
+            if evs is not None:
+                evs[i][0].record(stream)
+            call(s, lo, cnt)
+            if evs is not None:
+                evs[i][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in chunks] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local_rank)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    n_launch0 = iaat.iaat_launch_count()
+    t0.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    n_launch = iaat.iaat_launch_count() - n_launch0
+    clk = clocks.stop()
+    barrier(world)
+    ms_total = t0.elapsed_time(t1)
+    ms_total = allreduce_max(ms_total, world)
+    per_call_ms = np.zeros(len(chunks))
+    for k in range(args.steps):
+        for i, (a, b) in enumerate(evs[k]):
+            per_call_ms[i] += a.elapsed_time(b)
+    per_call_ms /= args.steps
+
+    flops_step = sum(s.flops(cnt) for s, lo, cnt in chunks)
+    ms_step = ms_total / args.steps
+    value = flops_step * world / (ms_step * 1e-3) / 1e9
+
+    # per-shape breakdown + dominant launch roofline
+    pk = peaks()
+    shapes_out = []
+    dom = int(np.argmax(per_call_ms))
+    for i, (s, lo, cnt) in enumerate(chunks):
+        t = per_call_ms[i] * 1e-3
+        gf = s.flops(cnt) / t / 1e9
+        t_roof = max(s.flops(cnt) / (FFMA_PEAK_TFLOPS * 1e12 if s.dtype == "f32" else DMMA_PEAK_TFLOPS * 1e12),
+                     s.alg_bytes(cnt) / (pk["hbm_gbs"] * 1e9))
+        shapes_out.append({"shape": s.name(), "batch": cnt, "us": round(t * 1e6, 2), "gflops": round(gf, 1),
+                           "hbm_gbs": round(s.alg_bytes(cnt) / t / 1e9, 1),
+                           "frac_roofline": round(t_roof / t, 4)})
+    s, lo, cnt = chunks[dom]
+    tdom = per_call_ms[dom] * 1e-3
+    hbm_time = s.alg_bytes(cnt) / (pk["hbm_gbs"] * 1e9)
+    cmp_peak = FFMA_PEAK_TFLOPS if s.dtype == "f32" else DMMA_PEAK_TFLOPS
+    cmp_time = s.flops(cnt) / (cmp_peak * 1e12)
+    traffic = load_traffic(s.name())
+    if hbm_time >= cmp_time:
+        roof = {"bound": "hbm", "achieved": round(s.alg_bytes(cnt) / tdom / 1e9, 1), "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": round(s.alg_bytes(cnt) / tdom / 1e9 / pk["hbm_gbs"], 4),
+                "traffic": traffic, "peak_source": pk["source"]}
+    else:
+        roof = {"bound": "alu", "achieved": round(s.flops(cnt) / tdom / 1e12, 2), "peak": round(cmp_peak, 1),
+                "unit": "TFLOP/s", "frac": round(s.flops(cnt) / tdom / 1e12 / cmp_peak, 4),
+                "traffic": traffic,
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md)"}
+    roof["kernel"] = s.name()
+    roof["share_of_step"] = round(per_call_ms[dom] / ms_step, 4)
+    roof["bytes_per_launch"] = s.alg_bytes(cnt)
+    roof["flops_per_launch"] = s.flops(cnt)
+
+    # --- e2e through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, chunks, bufs, call, stream, world)
+
+    line = {"metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if shapes[0].dtype == "f32" else "f64", "data": "synthetic",
+            "config": {"workload": desc, "calls_per_step": len(chunks),
+                       "l2": "inputs larger than L2: every call streams its own 256 MiB operand set "
+                             "(126 MB L2), no flush kernel needed" if args.config == 2 else
+                             "as workload states", "parallelism": "dp%d (batch shards, no collective)" % world},
+            "roofline": roof, "gpu_launches": int(n_launch), "clocks": clk, "e2e": e2e,
+            "shapes": shapes_out}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = run_cpu_baseline(shapes, args)
+    return line
+
+
+def run_chunked_config5(args, rank, world, local_rank, shapes, desc, chunks, bufs, call):
+    """Config 5 (fp64, up to 307 GB of operands per shape): chunks that fit
+    HBM; per chunk the inputs are generated (untimed) and the call timed with
+    CUDA events; GEMM time is summed."""
+    import torch
+    import datagen
+    from paper_2208_09822_b200 import iaat
+    tdt = torch.float64
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream()
+    res = {}
+    n_launch = 0
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    for s, lo, cnt in chunks:
+        key = (s.dtype, s.M, s.N, s.K, s.tr, cnt)
+        if key not in bufs:
+            bufs.clear()
+            torch.cuda.empty_cache()
+            ra, ca, rb, cb = s.stored()
+            bufs[key] = (torch.empty(cnt * ra * ca, dtype=tdt, device=dev),
+                         torch.empty(cnt * rb * cb, dtype=tdt, device=dev),
+                         torch.empty(cnt * s.M * s.N, dtype=tdt, device=dev))
+        A, B, C = bufs[key]
+        ra, ca, rb, cb = s.stored()
+        first = rank * s.batch + lo
+        datagen.fill_device(A, s.seed, datagen.MAT_A, ra, ca, ra, ra * ca, cnt, first)
+        datagen.fill_device(B, s.seed, datagen.MAT_B, rb, cb, rb, rb * cb, cnt, first)
+        for _ in range(args.warmup):
+            call(s, lo, cnt)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0 = iaat.iaat_launch_count()
+        e0.record(stream)
+        for _ in range(args.steps):
+            call(s, lo, cnt)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        n_launch += iaat.iaat_launch_count() - n0
+        res.setdefault(s.name(), [0.0, 0, s])
+        res[s.name()][0] += e0.elapsed_time(e1) / args.steps
+        res[s.name()][1] += cnt
+    clk = clocks.stop()
+    total_ms = sum(v[0] for v in res.values())
+    total_ms = allreduce_max(total_ms, world)
+    flops = sum(v[2].flops() for v in res.values())
+    value = flops * world / (total_ms * 1e-3) / 1e9
+    pk = peaks()
+    shapes_out = []
+    for nm, (ms, cnt, s) in res.items():
+        t = ms * 1e-3
+        t_roof = max(s.flops() / (DMMA_PEAK_TFLOPS * 1e12), s.alg_bytes() / (pk["hbm_gbs"] * 1e9))
+        shapes_out.append({"shape": nm, "batch": cnt, "ms": round(ms, 4), "gflops": round(s.flops() / t / 1e9, 1),
+                           "frac_roofline": round(t_roof / t, 4)})
+    return {"metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total_ms, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc}, "gpu_launches": int(n_launch), "clocks": clk, "shapes": shapes_out}
+
+
+def run_e2e(args, chunks, bufs, call, stream, world):
+    """Same sweep through the public C ABI, inputs from pinned host memory:
+    H2D of A, B, C and D2H of C per call are inside the timed region."""
+    import torch
+    host = {}
+    for key, (A, B, C) in bufs.items():
+        host[key] = tuple(t.cpu().pin_memory() for t in (A, B, C))
+    steps = max(1, min(args.steps, args.e2e_steps))
+
+    def step():
+        h2d = d2h = 0
+        for s, lo, cnt in chunks:
+            key = (s.dtype, s.M, s.N, s.K, s.tr, cnt)
+            (A, B, C), (hA, hB, hC) = bufs[key], host[key]
+            A.copy_(hA, non_blocking=True)
+            B.copy_(hB, non_blocking=True)
+            C.copy_(hC, non_blocking=True)
+            call(s, lo, cnt)
+            hC.copy_(C, non_blocking=True)
+            h2d += (A.numel() + B.numel() + C.numel()) * A.element_size()
+            d2h += C.numel() * C.element_size()
+        return h2d, d2h
+
+    step()
+    torch.cuda.synchronize()
+    barrier(world)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        h2d, d2h = step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = allreduce_max(t0.elapsed_time(t1) / steps, world)
+    flops = sum(s.flops(cnt) for s, lo, cnt in chunks)
+    return {"value": round(flops * world / (ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "ms_per_step": round(ms, 3)}
+
+
+# ---------------------------------------------------------------- CPU oracle (baseline / reference arm)
+def oracle_sample(shapes, frac):
+    out = []
+    for s in shapes:
+        out.append((s, max(1, int(s.batch * frac))))
+    return out
+
+
+def run_oracle_timed(shapes, frac, repeats=1):
+    import datagen
+    import oracle
+    dt = {"f32": np.float32, "f64": np.float64}
+    sample = oracle_sample(shapes, frac)
+    inputs = []
+    for s, n in sample:
+        ra, ca, rb, cb = s.stored()
+        ids = np.arange(n)
+        A = datagen.fill_host(s.seed, 0, dt[s.dtype], ra, ca, ra, ra * ca, ids)
+        B = datagen.fill_host(s.seed, 1, dt[s.dtype], rb, cb, rb, rb * cb, ids)
+        C = datagen.fill_host(s.seed, 2, dt[s.dtype], s.M, s.N, s.M, s.M * s.N, ids)
+        inputs.append((s, n, A, B, C))
+    total_t, total_f, threads = 0.0, 0.0, 0
+    for _ in range(repeats):
+        for s, n, A, B, C in inputs:
+            ra, ca, rb, cb = s.stored()
+            t = time.perf_counter()
+            _, _, threads = oracle.ref_gemm(s.tr[0], s.tr[1], s.M, s.N, s.K, s.alpha, A, ra, ra * ca, B, rb,
+                                            rb * cb, s.beta, C, s.M, s.M * s.N, n, want_den=False)
+            total_t += time.perf_counter() - t
+            total_f += s.flops(n)
+    return total_f / total_t / 1e9, threads, total_t
+
+
+def run_cpu_baseline(shapes, args):
+    frac = args.cpu_frac
+    gf, threads, t = run_oracle_timed(shapes, frac)
+    return {"value": round(gf, 3), "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+            "sample": "first %.4g of every shape's batch of the same step (all %d calls), fp64-accumulating "
+                      "C triple loop, OpenMP over problems; %.1f s of CPU time" % (frac, len(shapes), t)}
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return None
+    shapes, desc = workload(args.config)
+    frac = args.cpu_frac
+    run_oracle_timed(shapes, frac / 4)  # warm-up (untimed)
+    vals = []
+    t_all = 0.0
+    threads = 0
+    for _ in range(max(1, args.steps)):
+        gf, threads, t = run_oracle_timed(shapes, frac)
+        vals.append(gf)
+        t_all += t
+    value = float(np.median(vals))
+    sample = ("first %.4g of every shape's batch per step (%d calls), CPU oracle oracle/ref_gemm.c, "
+              "OpenMP over problems" % (frac, len(shapes)))
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_all / max(1, args.steps) * 1e3, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if shapes[0].dtype == "f32" else "f64", "data": "synthetic",
+            "config": {"workload": desc, "parallelism": "host cores (OpenMP)"},
+            "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+# ---------------------------------------------------------------- distributed plumbing
+_PG = None
+
+
+def init_dist():
+    global _PG
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+        _PG = dist
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1 and _PG is not None:
+        _PG.barrier()
+
+
+def allreduce_max(x, world):
+    if world > 1 and _PG is not None:
+        import torch
+        dev = "cuda" if torch.cuda.is_available() and _PG.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+        _PG.all_reduce(t, op=_PG.ReduceOp.MAX)
+        return float(t.item())
+    return float(x)
+
+
+def load_traffic(name):
+    """dram bytes per launch from a committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(name)
+    except Exception:
+        return None
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--cpu-frac", type=float, default=1.0 / 16)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args(argv)
+    rank, world, local = init_dist()
+    if args.impl == "reference":
+        line = run_reference_arm(args, rank, world)
+    else:
+        line = run_ours(args, rank, world, local)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1 and _PG is not None:
+        _PG.barrier()
+        _PG.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,383 @@
+// api.cu -- the C ABI of include/iaat.h (boundary row b of DESIGN.md).
+//
+// Validation and BLAS quick returns (row a1), plan cache (row a2), and the
+// single launch of the call's kernel executing plan on the caller's stream
+// (row a6).  There is no CPU fallback anywhere: a call
+// either enqueues sm_100a kernels or returns an error status.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "../../include/iaat.h"
+#include "iaat_device.cuh"
+#include "planner.h"
+
+#include "gen/kernel_table.inc"
+
+namespace iaat {
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+std::atomic<int64_t> g_launches{0};
+
+struct Key {
+    int64_t v[20];
+    bool operator==(const Key &o) const { return std::memcmp(v, o.v, sizeof v) == 0; }
+};
+struct KeyHash {
+    size_t operator()(const Key &k) const
+    {
+        uint64_t h = 1469598103934665603ull;
+        for (int64_t x : k.v) {
+            h ^= (uint64_t)x;
+            h *= 1099511628211ull;
+        }
+        return (size_t)h;
+    }
+};
+
+std::mutex g_mu;
+std::unordered_map<Key, Plan, KeyHash> g_cache;
+
+Key make_key(const PlanRequest &r)
+{
+    Key k;
+    std::memset(&k, 0, sizeof k);
+    int64_t *v = k.v;
+    v[0] = r.dtype;
+    v[1] = r.transA;
+    v[2] = r.transB;
+    v[3] = r.M;
+    v[4] = r.N;
+    v[5] = r.K;
+    v[6] = r.lda;
+    v[7] = r.ldb;
+    v[8] = r.ldc;
+    v[9] = r.sA;
+    v[10] = r.sB;
+    v[11] = r.sC;
+    v[12] = r.batch;
+    v[13] = r.beta_zero;
+    v[14] = r.alpha_zero;
+    v[15] = r.align;
+    v[16] = r.sm_count;
+    v[17] = r.ptr_array;
+    return k;
+}
+
+const Plan &cached_plan(const PlanRequest &r)
+{
+    Key k = make_key(r);
+    std::lock_guard<std::mutex> lock(g_mu);
+    auto it = g_cache.find(k);
+    if (it != g_cache.end()) return it->second;
+    if (g_cache.size() > 4096) g_cache.clear();
+    return g_cache.emplace(k, make_plan(r)).first->second;
+}
+
+struct DevInfo {
+    int sm_count = 0;
+    bool ok = false;
+};
+
+// Per-device: compute capability check (sm_100 only) and SM count.
+iaat_status_t device_info(DevInfo &out)
+{
+    static std::mutex mu;
+    static std::unordered_map<int, DevInfo> cache;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        g_last_cuda_error = (int)e;
+        return IAAT_ERROR_CUDA;
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(dev);
+    if (it == cache.end()) {
+        DevInfo d;
+        int major = 0, minor = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+            g_last_cuda_error = (int)cudaGetLastError();
+            return IAAT_ERROR_CUDA;
+        }
+        d.ok = (major == 10 && minor == 0);
+        it = cache.emplace(dev, d).first;
+    }
+    out = it->second;
+    return out.ok ? IAAT_SUCCESS : IAAT_ERROR_ARCH;
+}
+
+int parse_op(char c)
+{
+    if (c == 'N' || c == 'n') return 0;
+    if (c == 'T' || c == 't') return 1;
+    return -1;
+}
+
+int64_t max1(int64_t x) { return x > 1 ? x : 1; }
+
+// Row a1: argument validation + small-GEMM predicate.
+iaat_status_t validate(iaat_dtype_t dt, int ta, int tb, int64_t M, int64_t N, int64_t K, int64_t lda,
+                       int64_t ldb, int64_t ldc, int64_t batch, const void *alpha, const void *beta)
+{
+    if (dt != IAAT_R32F && dt != IAAT_R64F) return IAAT_ERROR_INVALID_VALUE;
+    if (ta < 0 || tb < 0) return IAAT_ERROR_INVALID_VALUE;
+    if (M < 0 || N < 0 || K < 0 || batch < 0) return IAAT_ERROR_INVALID_VALUE;
+    if (!alpha || !beta) return IAAT_ERROR_INVALID_VALUE;
+    const int64_t rowsA = ta ? K : M, rowsB = tb ? N : K;
+    if (lda < max1(rowsA) || ldb < max1(rowsB) || ldc < max1(M)) return IAAT_ERROR_INVALID_VALUE;
+    // ints inside the kernel: every ld and span must fit in 31 bits
+    if (lda > (1 << 30) || ldb > (1 << 30) || ldc > (1 << 30)) return IAAT_ERROR_NOT_SUPPORTED;
+    if (!iaat_is_small_gemm(ta ? 'T' : 'N', tb ? 'T' : 'N', M, N, K)) return IAAT_ERROR_NOT_SMALL;
+    return IAAT_SUCCESS;
+}
+
+double scalar(iaat_dtype_t dt, const void *p)
+{
+    return dt == IAAT_R32F ? (double)*static_cast<const float *>(p) : *static_cast<const double *>(p);
+}
+
+bool elem_aligned(const void *p, int elt) { return (reinterpret_cast<uintptr_t>(p) % elt) == 0; }
+
+// alpha == 0 or K == 0 path: C = beta * C (or zeros).  A/B never read.
+iaat_status_t launch_scale(iaat_dtype_t dt, char *C, void *const *Carr, int64_t sC, int64_t M, int64_t N,
+                           int64_t ldc, int64_t batch, double beta, cudaStream_t s, int sm_count)
+{
+    const int64_t total = M * N * batch;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > (int64_t)sm_count * 16) blocks = (int64_t)sm_count * 16;
+    if (dt == IAAT_R32F)
+        scale_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(C, Carr, sC, (int)M, (int)N, (int)ldc, batch, beta);
+    else
+        scale_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(C, Carr, sC, (int)M, (int)N, (int)ldc, batch, beta);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        g_last_cuda_error = (int)e;
+        return IAAT_ERROR_CUDA;
+    }
+    g_launches.fetch_add(1);
+    return IAAT_SUCCESS;
+}
+
+iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t N, int64_t K,
+                  const void *alpha, const void *A, int64_t lda, int64_t sA, const void *B, int64_t ldb,
+                  int64_t sB, const void *beta, void *C, int64_t ldc, int64_t sC, int64_t batch,
+                  const void *const *Aarr, const void *const *Barr, void *const *Carr, bool ptr_array,
+                  void *stream)
+{
+    const int ta = parse_op(transA), tb = parse_op(transB);
+    iaat_status_t st = validate(dt, ta, tb, M, N, K, lda, ldb, ldc, batch, alpha, beta);
+    if (st != IAAT_SUCCESS) return st;
+    const int elt = dt == IAAT_R32F ? 4 : 8;
+    if (!ptr_array && (sA < 0 || sB < 0 || sC < 0)) return IAAT_ERROR_INVALID_VALUE;
+    // C problems must not overlap (reading A18)
+    if (!ptr_array && batch > 1 && M > 0 && N > 0 && sC < (N - 1) * ldc + M) return IAAT_ERROR_INVALID_VALUE;
+    if (M == 0 || N == 0 || batch == 0) return IAAT_SUCCESS;  // nothing to do (reading A5)
+    const double a = scalar(dt, alpha), b = scalar(dt, beta);
+    const bool no_ab = (a == 0.0 || K == 0);
+    if (no_ab && b == 1.0) return IAAT_SUCCESS;  // C unchanged (reading A4)
+    if (ptr_array) {
+        if (!Carr || (!no_ab && (!Aarr || !Barr))) return IAAT_ERROR_INVALID_VALUE;
+    } else {
+        if (!C || (!no_ab && (!A || !B))) return IAAT_ERROR_INVALID_VALUE;
+        if (!elem_aligned(C, elt) || (!no_ab && (!elem_aligned(A, elt) || !elem_aligned(B, elt))))
+            return IAAT_ERROR_INVALID_VALUE;
+    }
+    DevInfo dev;
+    st = device_info(dev);
+    if (st != IAAT_SUCCESS) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (no_ab)
+        return launch_scale(dt, static_cast<char *>(C), Carr, sC, M, N, ldc, batch, b, s, dev.sm_count);
+
+    PlanRequest r;
+    r.dtype = dt == IAAT_R32F ? 0 : 1;
+    r.transA = ta;
+    r.transB = tb;
+    r.M = M;
+    r.N = N;
+    r.K = K;
+    r.lda = lda;
+    r.ldb = ldb;
+    r.ldc = ldc;
+    r.sA = ptr_array ? 0 : sA;
+    r.sB = ptr_array ? 0 : sB;
+    r.sC = ptr_array ? 0 : sC;
+    r.batch = batch;
+    r.beta_zero = b == 0.0;
+    r.alpha_zero = 0;
+    uintptr_t orr = ptr_array ? 0 : (reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
+                                     reinterpret_cast<uintptr_t>(C));
+    int64_t align = 256;
+    while (align > 1 && (orr % align)) align >>= 1;
+    r.align = ptr_array ? elt : align;
+    r.sm_count = dev.sm_count;
+    r.ptr_array = ptr_array ? 1 : 0;
+    const Plan &plan = cached_plan(r);
+    if (plan.status != 0) return (iaat_status_t)plan.status;
+
+    IaatKParams kp = plan.kp;
+    kp.A = static_cast<const char *>(A);
+    kp.B = static_cast<const char *>(B);
+    kp.C = static_cast<char *>(C);
+    kp.Aarr = Aarr;
+    kp.Barr = Barr;
+    kp.Carr = Carr;
+    kp.alpha = a;
+    kp.beta = b;
+    LaunchFn fn = kLaunch[r.dtype][ta * 2 + tb][plan.vec];
+    cudaError_t e = fn(kp, plan.grid, plan.block, plan.smem, s);
+    if (e != cudaSuccess) {
+        g_last_cuda_error = (int)e;
+        return IAAT_ERROR_CUDA;
+    }
+    g_launches.fetch_add(1);
+    return IAAT_SUCCESS;
+}
+
+}  // namespace
+}  // namespace iaat
+
+using namespace iaat;
+
+extern "C" {
+
+iaat_status_t iaat_gemm_strided_batched(iaat_dtype_t dtype, char transA, char transB, int64_t M, int64_t N,
+                                        int64_t K, const void *alpha, const void *A, int64_t lda,
+                                        int64_t strideA, const void *B, int64_t ldb, int64_t strideB,
+                                        const void *beta, void *C, int64_t ldc, int64_t strideC,
+                                        int64_t batch, void *stream)
+{
+    return run(dtype, transA, transB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc, strideC,
+               batch, nullptr, nullptr, nullptr, false, stream);
+}
+
+iaat_status_t iaat_gemm_batched(iaat_dtype_t dtype, char transA, char transB, int64_t M, int64_t N, int64_t K,
+                                const void *alpha, const void *const *Aarray, int64_t lda,
+                                const void *const *Barray, int64_t ldb, const void *beta,
+                                void *const *Carray, int64_t ldc, int64_t batch, void *stream)
+{
+    return run(dtype, transA, transB, M, N, K, alpha, nullptr, lda, 0, nullptr, ldb, 0, beta, nullptr, ldc, 0,
+               batch, Aarray, Barray, Carray, true, stream);
+}
+
+iaat_status_t iaat_sgemm_strided_batched(char transA, char transB, int64_t M, int64_t N, int64_t K, float alpha,
+                                         const float *A, int64_t lda, int64_t strideA, const float *B,
+                                         int64_t ldb, int64_t strideB, float beta, float *C, int64_t ldc,
+                                         int64_t strideC, int64_t batch, void *stream)
+{
+    return iaat_gemm_strided_batched(IAAT_R32F, transA, transB, M, N, K, &alpha, A, lda, strideA, B, ldb,
+                                     strideB, &beta, C, ldc, strideC, batch, stream);
+}
+
+iaat_status_t iaat_dgemm_strided_batched(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha,
+                                         const double *A, int64_t lda, int64_t strideA, const double *B,
+                                         int64_t ldb, int64_t strideB, double beta, double *C, int64_t ldc,
+                                         int64_t strideC, int64_t batch, void *stream)
+{
+    return iaat_gemm_strided_batched(IAAT_R64F, transA, transB, M, N, K, &alpha, A, lda, strideA, B, ldb,
+                                     strideB, &beta, C, ldc, strideC, batch, stream);
+}
+
+iaat_status_t iaat_sgemm_batched(char transA, char transB, int64_t M, int64_t N, int64_t K, float alpha,
+                                 const float *const *Aarray, int64_t lda, const float *const *Barray,
+                                 int64_t ldb, float beta, float *const *Carray, int64_t ldc, int64_t batch,
+                                 void *stream)
+{
+    return iaat_gemm_batched(IAAT_R32F, transA, transB, M, N, K, &alpha, (const void *const *)Aarray, lda,
+                             (const void *const *)Barray, ldb, &beta, (void *const *)Carray, ldc, batch, stream);
+}
+
+iaat_status_t iaat_dgemm_batched(char transA, char transB, int64_t M, int64_t N, int64_t K, double alpha,
+                                 const double *const *Aarray, int64_t lda, const double *const *Barray,
+                                 int64_t ldb, double beta, double *const *Carray, int64_t ldc, int64_t batch,
+                                 void *stream)
+{
+    return iaat_gemm_batched(IAAT_R64F, transA, transB, M, N, K, &alpha, (const void *const *)Aarray, lda,
+                             (const void *const *)Barray, ldb, &beta, (void *const *)Carray, ldc, batch, stream);
+}
+
+int iaat_is_small_gemm(char transA, char transB, int64_t M, int64_t N, int64_t K)
+{
+    // cbrt(MNK) <= 80, or <= 32 for TN -- integer form (reading A10)
+    const int ta = parse_op(transA), tb = parse_op(transB);
+    if (ta < 0 || tb < 0 || M < 0 || N < 0 || K < 0) return 0;
+    const int64_t lim = (ta == 1 && tb == 0) ? 32768 : 512000;
+    if (M == 0 || N == 0 || K == 0) return 1;
+    if (M > lim || N > lim || K > lim) return 0;
+    return M * N * K <= lim ? 1 : 0;
+}
+
+iaat_status_t iaat_plan_describe(iaat_dtype_t dtype, char transA, char transB, int64_t M, int64_t N, int64_t K,
+                                 int64_t lda, int64_t strideA, int64_t ldb, int64_t strideB, int64_t ldc,
+                                 int64_t strideC, int64_t batch, int beta_is_zero, int alpha_is_zero,
+                                 int64_t base_align_bytes, int sm_count, char *json, size_t cap)
+{
+    const int ta = parse_op(transA), tb = parse_op(transB);
+    double one = 1.0;
+    iaat_status_t st = validate(dtype, ta, tb, M, N, K, lda, ldb, ldc, batch, &one, &one);
+    if (st != IAAT_SUCCESS) return st;
+    if (!json || cap == 0 || sm_count <= 0 || M == 0 || N == 0 || K == 0 || batch == 0)
+        return IAAT_ERROR_INVALID_VALUE;
+    PlanRequest r;
+    r.dtype = dtype == IAAT_R32F ? 0 : 1;
+    r.transA = ta;
+    r.transB = tb;
+    r.M = M;
+    r.N = N;
+    r.K = K;
+    r.lda = lda;
+    r.ldb = ldb;
+    r.ldc = ldc;
+    r.sA = strideA;
+    r.sB = strideB;
+    r.sC = strideC;
+    r.batch = batch;
+    r.beta_zero = beta_is_zero ? 1 : 0;
+    r.alpha_zero = alpha_is_zero ? 1 : 0;
+    r.align = base_align_bytes;
+    r.sm_count = sm_count;
+    r.ptr_array = 0;
+    Plan p = make_plan(r);
+    std::string s = plan_json(r, p);
+    if (s.size() + 1 > cap) return IAAT_ERROR_INVALID_VALUE;
+    std::memcpy(json, s.c_str(), s.size() + 1);
+    return IAAT_SUCCESS;
+}
+
+iaat_status_t iaat_catalog_describe(char *json, size_t cap)
+{
+    const char *s = catalog_json();
+    size_t n = std::strlen(s);
+    if (!json || n + 1 > cap) return IAAT_ERROR_INVALID_VALUE;
+    std::memcpy(json, s, n + 1);
+    return IAAT_SUCCESS;
+}
+
+const char *iaat_status_string(iaat_status_t s)
+{
+    switch (s) {
+    case IAAT_SUCCESS: return "IAAT_SUCCESS";
+    case IAAT_ERROR_INVALID_VALUE: return "IAAT_ERROR_INVALID_VALUE";
+    case IAAT_ERROR_NOT_SMALL: return "IAAT_ERROR_NOT_SMALL";
+    case IAAT_ERROR_ARCH: return "IAAT_ERROR_ARCH";
+    case IAAT_ERROR_CUDA: return "IAAT_ERROR_CUDA";
+    case IAAT_ERROR_NOT_SUPPORTED: return "IAAT_ERROR_NOT_SUPPORTED";
+    }
+    return "IAAT_UNKNOWN_STATUS";
+}
+
+int iaat_last_cuda_error(void) { return g_last_cuda_error; }
+
+int64_t iaat_launch_count(void) { return g_launches.load(); }
+
+int iaat_version(void) { return 100; }
+
+}  // extern "C"

@@ -1,0 +1,152 @@
+// iaat_dmma.cuh -- fp64 warp tiles on the DMMA tensor-core path.
+//
+// fp64 is a genuine dense contraction, and on sm_100a the only FP64
+// tensor-core instruction is the legacy warp-level mma.sync.m8n8k4.f64
+// (SASS DMMA.8x8x4; tcgen05 has no f64 kind).  A warp owns a
+// (8*WM) x (8*WN) block of C and accumulates it in registers over the whole K
+// of the problem -- the warp-level analogue of the paper's register-blocked
+// kernel (Alg. 1: Cregs hold the whole C_c block while
+// columns of A_c and rows of B_c stream through).
+//
+// The MMA is issued in transposed form, D' = op(B)^T op(A)^T (= C^T), so a
+// lane's two accumulator elements are two CONSECUTIVE ROWS of one column of
+// the column-major C (one 16-byte store) -- PAPER.md:312 "SIMD friendly".
+//   A' fragment (8x4, row): lane (g = lane/4, t = lane%4) holds
+//        A'(g, t) = op(B)(k0+t, col0+g)
+//   B' fragment (4x8, col): lane holds B'(t, g) = op(A)(row0+g, k0+t)
+//   D' (8x8): lane holds D'(g, 2t+h) = C(row0 + 2t + h, col0 + g), h = 0, 1
+// K % 4 tail: the missing k of the last step are zero in BOTH fragments
+// (0*0 adds nothing); no MMA is predicated.
+#pragma once
+#include "iaat_device.cuh"
+
+namespace iaat {
+
+__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <bool TA, bool TB, int WM, int WN>
+__device__ __forceinline__ void dmma_tile(double (&acc)[WM][WN][2], const double *__restrict__ sA,
+                                          const double *__restrict__ sB, int lda, int ldb, int K,
+                                          int row0, int col0, int g, int t)
+{
+    // element addresses relative to k = 0
+    int aoff[WM], boff[WN];
+#pragma unroll
+    for (int mi = 0; mi < WM; ++mi) {
+        const int r = row0 + 8 * mi + g;
+        aoff[mi] = TA ? (t + r * lda) : (r + t * lda);
+    }
+#pragma unroll
+    for (int nj = 0; nj < WN; ++nj) {
+        const int cidx = col0 + 8 * nj + g;
+        boff[nj] = TB ? (cidx + t * ldb) : (t + cidx * ldb);
+    }
+    const int astep = TA ? 4 : 4 * lda;  // address step per k-step of 4
+    const int bstep = TB ? 4 * ldb : 4;
+    const int kfull = K & ~3;
+    int k0 = 0;
+#pragma unroll 2
+    for (; k0 < kfull; k0 += 4) {
+        double af[WM], bf[WN];
+#pragma unroll
+        for (int mi = 0; mi < WM; ++mi) af[mi] = sA[aoff[mi]];
+#pragma unroll
+        for (int nj = 0; nj < WN; ++nj) bf[nj] = sB[boff[nj]];
+#pragma unroll
+        for (int mi = 0; mi < WM; ++mi) aoff[mi] += astep;
+#pragma unroll
+        for (int nj = 0; nj < WN; ++nj) boff[nj] += bstep;
+#pragma unroll
+        for (int mi = 0; mi < WM; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < WN; ++nj) dmma_8x8x4(acc[mi][nj][0], acc[mi][nj][1], bf[nj], af[mi]);
+    }
+    if (k0 < K) {  // K % 4 tail: zero-fill the k >= K lanes of both fragments
+        const bool valid = k0 + t < K;
+        double af[WM], bf[WN];
+#pragma unroll
+        for (int mi = 0; mi < WM; ++mi) af[mi] = valid ? sA[aoff[mi]] : 0.0;
+#pragma unroll
+        for (int nj = 0; nj < WN; ++nj) bf[nj] = valid ? sB[boff[nj]] : 0.0;
+#pragma unroll
+        for (int mi = 0; mi < WM; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < WN; ++nj) dmma_8x8x4(acc[mi][nj][0], acc[mi][nj][1], bf[nj], af[mi]);
+    }
+}
+
+// One compute warp running DMMA class `c`: the class' warps share the
+// group's (problem, warp-tile) items round-robin.
+template <bool TA, bool TB, int WM, int WN, bool VEC>
+__device__ __forceinline__ void dmma_class_loop(const IaatKParams &p, const IaatClass &c,
+                                                unsigned char *smem, uint64_t *full,
+                                                uint64_t *empty, int warp, int lane)
+{
+    const int g = lane >> 2, t = lane & 3;
+    const int nw = c.warp_end - c.warp_begin, wi = warp - c.warp_begin;
+    const double alpha = p.alpha, beta = p.beta;
+    const int64_t sab = p.sA * 8, sbb = p.sB * 8, scb = p.sC * 8;
+    int it = 0;
+    for (int64_t gr = blockIdx.x; gr < p.ngroups; gr += gridDim.x, ++it) {
+        const int s = it % p.S;
+        const int64_t b0 = gr * p.P;
+        const int np = (int)min((int64_t)p.P, p.batch - b0);
+        mbar_wait(&full[s], (it / p.S) & 1);
+        StageView sv = stage_view(p, smem, s);
+        const char *a_first = prob_ptr(p.A, p.Aarr, sab, b0);
+        const char *b_first = prob_ptr(p.B, p.Barr, sbb, b0);
+        const int items = np * c.tiles;
+        for (int item = wi; item < items; item += nw) {
+            const int pl = item / c.tiles, tt = item - pl * c.tiles;
+            const int ti = tt % c.tm, tj = tt / c.tm;
+            const int row0 = c.row_base + ti * 8 * WM, col0 = c.col_base + tj * 8 * WN;
+            const char *a_prob = p.modeA == IAAT_STAGE_SLAB ? a_first : prob_ptr(p.A, p.Aarr, sab, b0 + pl);
+            const char *b_prob = p.modeB == IAAT_STAGE_SLAB ? b_first : prob_ptr(p.B, p.Barr, sbb, b0 + pl);
+            const double *sA = reinterpret_cast<const double *>(
+                sv.a + smem_offset(p.modeA, a_first, a_prob, sab, p.slotA, pl));
+            const double *sB = reinterpret_cast<const double *>(
+                sv.b + smem_offset(p.modeB, b_first, b_prob, sbb, p.slotB, pl));
+            double acc[WM][WN][2];
+#pragma unroll
+            for (int mi = 0; mi < WM; ++mi)
+#pragma unroll
+                for (int nj = 0; nj < WN; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+            dmma_tile<TA, TB, WM, WN>(acc, sA, sB, p.lda, p.ldb, p.K, row0, col0, g, t);
+            double *C = p.Carr ? reinterpret_cast<double *>(p.Carr[b0 + pl])
+                               : reinterpret_cast<double *>(p.C + (b0 + pl) * scb);
+#pragma unroll
+            for (int mi = 0; mi < WM; ++mi)
+#pragma unroll
+                for (int nj = 0; nj < WN; ++nj) {
+                    double *cp = C + (row0 + 8 * mi + 2 * t) + (int64_t)(col0 + 8 * nj + g) * p.ldc;
+                    double o[2];
+                    if (VEC) {
+                        if (p.beta_zero) {
+                            o[0] = mul_rn(alpha, acc[mi][nj][0]);
+                            o[1] = mul_rn(alpha, acc[mi][nj][1]);
+                        } else {
+                            double ci[2];
+                            ld_vec<double>(cp, ci);
+                            o[0] = fma_rn(alpha, acc[mi][nj][0], mul_rn(beta, ci[0]));
+                            o[1] = fma_rn(alpha, acc[mi][nj][1], mul_rn(beta, ci[1]));
+                        }
+                        st_vec<double>(cp, o);
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            cp[h] = p.beta_zero ? mul_rn(alpha, acc[mi][nj][h])
+                                                : fma_rn(alpha, acc[mi][nj][h], mul_rn(beta, cp[h]));
+                    }
+                }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+}
+
+}  // namespace iaat

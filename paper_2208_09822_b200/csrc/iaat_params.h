@@ -1,0 +1,70 @@
+// iaat_params.h -- the "kernel executing plan" (Sec. V-B)
+// as it crosses the host->device boundary: one POD struct passed by value
+// (__grid_constant__) to the single persistent launch of a call.
+//
+// Host (planner.cpp, api.cu) and device (iaat_device.cuh) both include this.
+#pragma once
+#include <stdint.h>
+
+#define IAAT_MAX_CLASSES 4
+#define IAAT_MAX_STAGES 6
+#define IAAT_MAX_THREADS 512          // __launch_bounds__ of every pipeline kernel
+#define IAAT_MAX_COMPUTE_WARPS 15     // + 1 producer warp
+#define IAAT_SMEM_LIMIT (227 * 1024)  // opt-in dynamic shared memory per CTA
+#define IAAT_BAR_BYTES 128            // mbarriers live in the first 128 B
+
+// Staging modes for an operand.
+enum IaatStage : int {
+    IAAT_STAGE_SLAB = 0,     // one bulk copy of the enclosing 16 B-aligned span of P problems
+    IAAT_STAGE_PERPROB = 1,  // one bulk copy per problem into its own smem slot
+};
+
+// Micro-tile families of the install-time catalog.
+enum IaatFamily : int {
+    IAAT_FAM_FMA = 0,   // per-thread mr x nr FFMA/DFMA register tile
+    IAAT_FAM_DMMA = 1,  // per-warp (8*wm) x (8*wn) DMMA.8x8x4 tile (fp64 only)
+};
+
+// One tile class: all tiles of one exact size (mr x nr) inside one row strip
+// and one column strip of C (Alg. 2 "blocksC", "m[]", "n[]").
+// Warps [warp_begin, warp_end) run it; lane index -> (problem, tile).
+struct IaatClass {
+    int code;        // catalog entry (dispatch switch case), see catalog.inc
+    int warp_begin;  // first compute warp of this class
+    int warp_end;    // one past the last
+    int tiles;       // tiles of this class per problem (= tm * tn)
+    int tm;          // tiles along M inside the class (row-fastest tile order)
+    int row_base;    // first row of the class' row strip
+    int mr;          // tile rows (== the catalog entry's MR; kept for host printing)
+    int col_base;    // first column of the class' column strip
+    int nr;          // tile columns
+    int units;       // lanes (FMA family) or warps (DMMA family) per problem
+};
+
+struct IaatKParams {
+    // strided API: byte base pointers; pointer-array API: the arrays (else null)
+    const char *A;
+    const char *B;
+    char *C;
+    const void *const *Aarr;
+    const void *const *Barr;
+    void *const *Carr;
+    int64_t sA, sB, sC;  // strides in elements (strided API)
+    int64_t batch;       // problems in this call
+    int64_t ngroups;     // ceil(batch / P)
+    double alpha, beta;
+    int M, N, K;
+    int lda, ldb, ldc;
+    int P;               // problems per group (one pipeline stage)
+    int S;               // pipeline stages
+    int n_compute_warps;
+    int modeA, modeB;    // IaatStage
+    int spanA, spanB;    // bytes spanned by one problem's A / B
+    int slotA, slotB;    // per-problem smem slot (PERPROB mode), bytes
+    int capA, capB;      // smem bytes reserved per stage for A / B (multiple of 128)
+    int stage_bytes;     // capA + capB
+    int beta_zero;       // 1: C is write-only
+    int prefetch_c;      // 1: producer prefetches the C span into L2
+    int nclasses;
+    IaatClass cls[IAAT_MAX_CLASSES];
+};

@@ -1,0 +1,55 @@
+// planner.h -- run-time stage: input-aware planning of one batched call
+// (Sec. III-B / V).
+#pragma once
+#include <stdint.h>
+
+#include <string>
+
+#include "iaat_params.h"
+
+namespace iaat {
+
+struct PlanRequest {
+    int dtype;          // 0 fp32, 1 fp64
+    int transA, transB; // 0 = N, 1 = T
+    int64_t M, N, K;
+    int64_t lda, ldb, ldc;
+    int64_t sA, sB, sC; // strides (elements); ignored for the pointer-array API
+    int64_t batch;
+    int beta_zero, alpha_zero;
+    int64_t align;      // common alignment (bytes) of the A/B/C base addresses
+    int sm_count;
+    int ptr_array;      // 1 = iaat_gemm_batched
+};
+
+// One strip of a 1-D decomposition (Alg. 2's (dim, nums) pairs).
+struct Strip {
+    int size;
+    int count;
+};
+
+struct Plan {
+    int status = 0;        // iaat_status_t (SUCCESS or NOT_SUPPORTED)
+    IaatKParams kp{};      // pointers / alpha / beta filled at call time
+    int grid = 0, block = 0, smem = 0;
+    int vec = 0;           // kernel variant: 16-byte vector paths enabled
+    int family = 0;        // IAAT_FAM_FMA or IAAT_FAM_DMMA
+    Strip mstrip[2]{}, nstrip[2]{};
+    int nm = 0, nn = 0;    // strips used per dimension
+    int64_t memops = 0;    // paper cost: sum_i (m_i + n_i) K + 2 M N
+    double est_cycles = 0; // modelled SM cycles per group
+    double est_total = 0;  // modelled cycles for the whole call
+};
+
+// Build the plan (pure host function; no CUDA calls).
+Plan make_plan(const PlanRequest &r);
+
+// JSON description (iaat_plan_describe).
+std::string plan_json(const PlanRequest &r, const Plan &p);
+
+// True if (dtype, trans, family, mr, nr) is in the install-time catalog.
+bool catalog_has(int dtype, int trans_idx, int family, int mr, int nr);
+int catalog_code(int family, int mr, int nr);
+const char *catalog_json();
+
+}  // namespace iaat

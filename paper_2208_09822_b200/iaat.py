@@ -1,0 +1,167 @@
+"""Thin ctypes binding of include/iaat.h (argument marshalling only).
+
+Every name mirrors the C ABI.  No arithmetic happens here: each call goes
+straight into libiaat.so, which enqueues sm_100a kernels or returns an error
+status.  If the library is missing the import fails loudly -- there is no
+CPU fallback.  Torch is used only to obtain device pointers and the current
+stream in the convenience wrappers at the bottom.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libiaat.so")
+
+IAAT_R32F, IAAT_R64F = 0, 1
+STATUS = {
+    0: "IAAT_SUCCESS",
+    1: "IAAT_ERROR_INVALID_VALUE",
+    2: "IAAT_ERROR_NOT_SMALL",
+    3: "IAAT_ERROR_ARCH",
+    4: "IAAT_ERROR_CUDA",
+    5: "IAAT_ERROR_NOT_SUPPORTED",
+}
+
+# exported symbols of include/iaat.h (tests check the .so exports exactly these)
+EXPORTS = [
+    "iaat_gemm_strided_batched", "iaat_gemm_batched",
+    "iaat_sgemm_strided_batched", "iaat_dgemm_strided_batched",
+    "iaat_sgemm_batched", "iaat_dgemm_batched",
+    "iaat_is_small_gemm", "iaat_plan_describe", "iaat_catalog_describe",
+    "iaat_status_string", "iaat_last_cuda_error", "iaat_launch_count", "iaat_version",
+]
+
+
+class IaatError(RuntimeError):
+    def __init__(self, status, what=""):
+        self.status = status
+        super().__init__("%s%s" % (STATUS.get(status, status), (": " + what) if what else ""))
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError("libiaat.so not built (%s): run `python -m paper_2208_09822_b200.build` "
+                          "-- there is no CPU fallback" % LIB_PATH)
+    lib = ctypes.CDLL(LIB_PATH)
+    i64, vp, c, i = ctypes.c_int64, ctypes.c_void_p, ctypes.c_char, ctypes.c_int
+    lib.iaat_gemm_strided_batched.argtypes = [i, c, c, i64, i64, i64, vp, vp, i64, i64, vp, i64, i64,
+                                              vp, vp, i64, i64, i64, vp]
+    lib.iaat_gemm_strided_batched.restype = i
+    lib.iaat_gemm_batched.argtypes = [i, c, c, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, i64, i64, vp]
+    lib.iaat_gemm_batched.restype = i
+    lib.iaat_is_small_gemm.argtypes = [c, c, i64, i64, i64]
+    lib.iaat_is_small_gemm.restype = i
+    lib.iaat_plan_describe.argtypes = [i, c, c, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i, i,
+                                       i64, i, ctypes.c_char_p, ctypes.c_size_t]
+    lib.iaat_plan_describe.restype = i
+    lib.iaat_catalog_describe.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
+    lib.iaat_catalog_describe.restype = i
+    lib.iaat_status_string.argtypes = [i]
+    lib.iaat_status_string.restype = ctypes.c_char_p
+    lib.iaat_last_cuda_error.restype = i
+    lib.iaat_launch_count.restype = i64
+    lib.iaat_version.restype = i
+    return lib
+
+
+_lib = _load()
+
+
+def _ch(x):
+    return x.encode() if isinstance(x, str) else bytes([x]) if isinstance(x, int) else x
+
+
+def _scalar(dtype, v):
+    return ctypes.byref(ctypes.c_float(v) if dtype == IAAT_R32F else ctypes.c_double(v))
+
+
+# ---------------------------------------------------------------- C-ABI mirrors
+def iaat_gemm_strided_batched(dtype, transA, transB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
+                              beta, C, ldc, strideC, batch, stream=0):
+    """A, B, C, stream: integer device addresses / cudaStream_t.  alpha,
+    beta: Python floats (passed as host scalars of `dtype`).  Returns status."""
+    return _lib.iaat_gemm_strided_batched(dtype, _ch(transA), _ch(transB), M, N, K, _scalar(dtype, alpha),
+                                          A, lda, strideA, B, ldb, strideB, _scalar(dtype, beta), C, ldc,
+                                          strideC, batch, stream)
+
+
+def iaat_gemm_batched(dtype, transA, transB, M, N, K, alpha, Aarray, lda, Barray, ldb, beta, Carray, ldc,
+                      batch, stream=0):
+    """Aarray/Barray/Carray: integer DEVICE addresses of device pointer arrays."""
+    return _lib.iaat_gemm_batched(dtype, _ch(transA), _ch(transB), M, N, K, _scalar(dtype, alpha), Aarray,
+                                  lda, Barray, ldb, _scalar(dtype, beta), Carray, ldc, batch, stream)
+
+
+def iaat_is_small_gemm(transA, transB, M, N, K) -> bool:
+    return bool(_lib.iaat_is_small_gemm(_ch(transA), _ch(transB), M, N, K))
+
+
+def iaat_plan_describe(dtype, transA, transB, M, N, K, lda, strideA, ldb, strideB, ldc, strideC, batch,
+                       beta_is_zero=False, alpha_is_zero=False, base_align_bytes=256, sm_count=148):
+    buf = ctypes.create_string_buffer(16384)
+    st = _lib.iaat_plan_describe(dtype, _ch(transA), _ch(transB), M, N, K, lda, strideA, ldb, strideB, ldc,
+                                 strideC, batch, int(beta_is_zero), int(alpha_is_zero), base_align_bytes,
+                                 sm_count, buf, len(buf))
+    if st != 0:
+        raise IaatError(st, "iaat_plan_describe")
+    return json.loads(buf.value.decode())
+
+
+def iaat_catalog_describe():
+    buf = ctypes.create_string_buffer(1 << 20)
+    st = _lib.iaat_catalog_describe(buf, len(buf))
+    if st != 0:
+        raise IaatError(st, "iaat_catalog_describe")
+    return json.loads(buf.value.decode())
+
+
+def iaat_status_string(status) -> str:
+    return _lib.iaat_status_string(status).decode()
+
+
+def iaat_last_cuda_error() -> int:
+    return _lib.iaat_last_cuda_error()
+
+
+def iaat_launch_count() -> int:
+    return _lib.iaat_launch_count()
+
+
+def iaat_version() -> int:
+    return _lib.iaat_version()
+
+
+# ---------------------------------------------------------------- torch convenience
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def gemm_strided_batched(transA, transB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB, beta, C, ldc,
+                         strideC, batch, stream=None, check=True):
+    """Same call with torch CUDA tensors (float32 or float64, flat or any
+    shape; only data_ptr() is used).  Raises IaatError on a non-success
+    status when check=True."""
+    import torch
+    dtype = {torch.float32: IAAT_R32F, torch.float64: IAAT_R64F}[C.dtype]
+    st = iaat_gemm_strided_batched(dtype, transA, transB, M, N, K, alpha, A.data_ptr(), lda, strideA,
+                                   B.data_ptr(), ldb, strideB, beta, C.data_ptr(), ldc, strideC, batch,
+                                   _stream_handle(stream))
+    if check and st != 0:
+        raise IaatError(st, "cuda error %d" % iaat_last_cuda_error() if st == 4 else "")
+    return st
+
+
+def gemm_batched(transA, transB, M, N, K, alpha, Aptrs, lda, Bptrs, ldb, beta, Cptrs, ldc, batch,
+                 dtype, stream=None, check=True):
+    """Aptrs/Bptrs/Cptrs: int64 CUDA tensors holding device addresses."""
+    st = iaat_gemm_batched(dtype, transA, transB, M, N, K, alpha, Aptrs.data_ptr(), lda, Bptrs.data_ptr(),
+                           ldb, beta, Cptrs.data_ptr(), ldc, batch, _stream_handle(stream))
+    if check and st != 0:
+        raise IaatError(st, "cuda error %d" % iaat_last_cuda_error() if st == 4 else "")
+    return st

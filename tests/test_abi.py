@@ -1,0 +1,60 @@
+"""CPU-side checks of the C ABI: the library loads without a GPU, exports
+every symbol include/iaat.h declares, and the host-only entry points
+(predicate, planner description, catalog) behave."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "iaat.h")
+
+
+def header_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(iaat_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2208_09822_b200 import iaat
+    declared = header_functions()
+    assert set(declared) == set(iaat.EXPORTS)
+    out = subprocess.run(["nm", "-D", "--defined-only", iaat.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\sT\s(iaat_\w+)", out))
+    missing = set(declared) - exported
+    assert not missing, missing
+    lib = ctypes.CDLL(iaat.LIB_PATH)
+    for name in declared:
+        assert getattr(lib, name)
+
+
+def test_small_predicate_matches_paper_examples():
+    import json
+    from paper_2208_09822_b200 import iaat
+    cases = json.load(open(os.path.join(ROOT, "tests", "golden", "predicate.json")))["cases"]
+    for c in cases:
+        assert iaat.iaat_is_small_gemm(c["transA"], c["transB"], c["M"], c["N"], c["K"]) == c["small"], c
+    assert not iaat.iaat_is_small_gemm("C", "N", 2, 2, 2)
+    assert not iaat.iaat_is_small_gemm("N", "N", -1, 2, 2)
+
+
+def test_status_strings_and_version():
+    from paper_2208_09822_b200 import iaat
+    for k, v in iaat.STATUS.items():
+        assert iaat.iaat_status_string(k) == v
+    assert iaat.iaat_version() >= 100
+
+
+def test_no_gpu_call_fails_cleanly():
+    """Without a GPU a valid call returns a status (never crashes, never
+    computes on the CPU)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2208_09822_b200 import iaat
+    st = iaat.iaat_gemm_strided_batched(0, "N", "N", 4, 4, 4, 1.0, 256, 4, 16, 512, 4, 16, 0.0, 1024, 4, 16, 2)
+    assert st in (3, 4)
+    assert iaat.iaat_status_string(st).startswith("IAAT_ERROR")

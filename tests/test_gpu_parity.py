@@ -1,0 +1,347 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Element-wise, on seeded inputs, within north_star's tolerances (1e-5 fp32,
+1e-13 fp64, normalised by |alpha||opA||opB| + |beta||C|); bitwise where the
+arithmetic is exact (integer-valued inputs, P4) or where the design fixes it
+(determinism, batch-split invariance, fp32 transpose identity).
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+import pytest
+
+from tests.gpu_utils import Case, TOL, config2_batch, config3_shapes, config4_shapes, sample_ids
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2208_09822_b200 import iaat  # noqa: F401  (fails loudly if not built)
+    yield
+
+
+F32, F64 = np.float32, np.float64
+TRANS = ["NN", "NT", "TN", "TT"]
+
+
+def bits_equal(a, b):
+    """Bitwise tensor equality (NaN payloads included)."""
+    it = torch.int32 if a.dtype == torch.float32 else torch.int64
+    return torch.equal(a.view(it), b.view(it))
+
+
+# ---------------------------------------------------------------- datagen twin
+def test_datagen_gpu_twin_bitwise():
+    import datagen
+    for dt, tdt in ((F32, torch.float32), (F64, torch.float64)):
+        t = torch.empty(3 * 45, dtype=tdt, device="cuda")
+        datagen.fill_device(t, 7, datagen.MAT_B, 5, 6, 7, 45, 3, first_id=11)
+        want = datagen.fill_host(7, datagen.MAT_B, dt, 5, 6, 7, 45, [11, 12, 13])
+        got = t.cpu().numpy()
+        assert np.array_equal(np.isnan(got), np.isnan(want))
+        m = ~np.isnan(want)
+        assert np.array_equal(got[m].view(np.uint8), want[m].view(np.uint8))
+
+
+# ---------------------------------------------------------------- brute force 1..4^3
+@pytest.mark.parametrize("dtype", [F32, F64])
+@pytest.mark.parametrize("tr", TRANS)
+def test_brute_force_small(dtype, tr):
+    """P8: every (M,N,K) in {1..4}^3, this transposition, several alpha/beta,
+    minimal and padded ld (NaN sentinels in the padding and between problems)."""
+    ab = [(1.0, 0.0), (1.5, 0.5), (-1.0, 1.0), (0.5, -1.0)]
+    for (M, N, K), (alpha, beta), pad in itertools.product(itertools.product(range(1, 5), repeat=3), ab, (0, 3)):
+        c = Case(dtype, tr[0], tr[1], M, N, K, 5, 100 + M * 16 + N * 4 + K, alpha, beta, pad=pad, spad=pad)
+        c.run()
+        c.check()
+
+
+# ---------------------------------------------------------------- configs (reduced batch, every problem)
+@pytest.mark.parametrize("tr", ["NN", "NT", "TT"])
+def test_config2_square_sweep(tr):
+    for n in range(4, 81, 4):
+        c = Case(F32, tr[0], tr[1], n, n, n, 600, 1, 1.5, 0.5)
+        c.run()
+        c.check()
+
+
+def test_config1_full():
+    c = Case(F32, "N", "N", 16, 16, 16, 2000, 0, 1.0, 0.0)
+    c.run()
+    c.check()
+
+
+def test_config3_irregular():
+    for (M, N, K) in config3_shapes():
+        c = Case(F32, "N", "N", M, N, K, 300, 2, 1.0, 1.0)
+        c.run()
+        c.check()
+
+
+@pytest.mark.parametrize("tr", ["NT", "TT"])
+def test_config3_irregular_other_trans(tr):
+    for (M, N, K) in config3_shapes()[::4]:
+        c = Case(F32, tr[0], tr[1], M, N, K, 200, 2, 1.0, 1.0)
+        c.run()
+        c.check()
+
+
+def test_config4_tn():
+    for (M, N, K) in config4_shapes():
+        c = Case(F32, "T", "N", M, N, K, 1000, 3, -1.0, 0.25)
+        c.run()
+        c.check()
+
+
+@pytest.mark.parametrize("tr", ["NN", "NT"])
+def test_config5_fp64(tr):
+    for n in (8, 16, 32, 48, 64, 80):
+        c = Case(F64, tr[0], tr[1], n, n, n, 400, 4, 1.0, 0.0)
+        c.run()
+        c.check()
+
+
+@pytest.mark.parametrize("tr", ["TN", "TT"])
+def test_fp64_other_trans(tr):
+    for (M, N, K) in [(8, 8, 8), (16, 24, 13), (31, 17, 23), (32, 32, 32)]:
+        c = Case(F64, tr[0], tr[1], M, N, K, 300, 40, 1.5, -0.5)
+        c.run()
+        c.check()
+
+
+def test_fp64_odd_shapes():
+    for (M, N, K) in [(7, 9, 11), (23, 5, 41), (79, 79, 79), (1, 80, 80), (80, 1, 3), (13, 64, 7)]:
+        for tr in TRANS:
+            if tr == "TN" and M * N * K > 32768:
+                continue
+            c = Case(F64, tr[0], tr[1], M, N, K, 64, 41, 1.0, 1.0)
+            c.run()
+            c.check()
+
+
+# ---------------------------------------------------------------- full-size launch configs, sampled
+@pytest.mark.parametrize("n", [4, 16, 32, 64, 80])
+def test_config2_full_batch_sampled(n):
+    """The bench's launch configuration (config 2 full batch), checked on the
+    first/last 256 problems and 1024 seeded random ones."""
+    c = Case(F32, "N", "N", n, n, n, config2_batch(n), 1, 1.5, 0.5)
+    c.run()
+    c.check(sample_ids(c.batch))
+
+
+def test_config5_full_batch_sampled():
+    c = Case(F64, "N", "N", 32, 32, 32, 2_000_000, 4, 1.0, 0.0)
+    c.run()
+    c.check(sample_ids(c.batch))
+
+
+# ---------------------------------------------------------------- exactness / invariants
+@pytest.mark.parametrize("dtype", [F32, F64])
+@pytest.mark.parametrize("tr", TRANS)
+def test_integer_inputs_bitwise(dtype, tr):
+    """P4: integer entries -> every product and partial sum is exact, so the
+    GPU equals the (exact) oracle bitwise for any summation order."""
+    from paper_2208_09822_b200 import iaat
+    rng = np.random.default_rng(44)
+    M, N, K, batch = 13, 11, 30, 50
+    ra, ca = (M, K) if tr[0] == "N" else (K, M)
+    rb, cb = (K, N) if tr[1] == "N" else (N, K)
+    A = rng.integers(-8, 9, batch * ra * ca).astype(dtype)
+    B = rng.integers(-8, 9, batch * rb * cb).astype(dtype)
+    C = rng.integers(-8, 9, batch * M * N).astype(dtype)
+    import oracle
+    ref, _, _ = oracle.ref_gemm(tr[0], tr[1], M, N, K, 0.5, A, ra, ra * ca, B, rb, rb * cb, -1.5, C, M, M * N, batch)
+    dA, dB, dC = (torch.from_numpy(x).cuda() for x in (A, B, C))
+    iaat.gemm_strided_batched(tr[0], tr[1], M, N, K, 0.5, dA, ra, ra * ca, dB, rb, rb * cb, -1.5, dC, M, M * N, batch)
+    got = dC.cpu().numpy().astype(np.float64).reshape(batch, N, M)
+    assert np.array_equal(got, ref)
+
+
+def test_transpose_identity_fp32_bitwise():
+    """P7: op(A)op(B) = (op(B)^T op(A)^T)^T -- one k-ascending FFMA chain per
+    element and fma(a,b,c) = fma(b,a,c) make the two calls bitwise equal."""
+    from paper_2208_09822_b200 import iaat
+    flip = {"N": "T", "T": "N"}
+    for tr in TRANS:
+        M, N, K, batch = 19, 12, 37, 40
+        c1 = Case(F32, tr[0], tr[1], M, N, K, batch, 77, 1.0, 0.0)
+        c1.run()
+        A, B, _ = c1.views()
+        C2 = torch.empty(batch * N * M, dtype=torch.float32, device="cuda")
+        iaat.gemm_strided_batched(flip[tr[1]], flip[tr[0]], N, M, K, 1.0, B, c1.ldb, c1.sB, A, c1.lda, c1.sA,
+                                  0.0, C2, N, N * M, batch)
+        g1 = c1.gpu_result(np.arange(batch))
+        # C2 is N x M column-major (ldc = N): C2[b][i*N + j] = C2(j, i) = C(i, j)
+        g2 = C2.view(batch, M, N).double().cpu().numpy().transpose(0, 2, 1)
+        assert np.array_equal(g1, g2), tr
+
+
+def test_determinism_and_batch_split_invariance():
+    """P11: two runs and a 3-way split of the batch give bitwise equal C."""
+    from paper_2208_09822_b200 import iaat
+    for dtype, n in ((F32, 24), (F64, 32)):
+        c = Case(dtype, "N", "T", n, n, n, 3001, 9, 1.0, 0.0)
+        c.run()
+        r1 = c.views()[2].clone()
+        c.run()
+        assert bits_equal(r1, c.views()[2])
+        A, B, C = c.views()
+        C.fill_(float("nan"))
+        cuts = [0, 1000, 1777, 3001]
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            iaat.gemm_strided_batched("N", "T", n, n, n, 1.0, A[lo * c.sA:], c.lda, c.sA, B[lo * c.sB:], c.ldb,
+                                      c.sB, 0.0, C[lo * c.sC:], c.ldc, c.sC, hi - lo)
+        assert bits_equal(r1, C)
+
+
+def test_beta_zero_ignores_nan_c_and_alpha_zero_ignores_ab():
+    from paper_2208_09822_b200 import iaat
+    c = Case(F32, "N", "N", 9, 7, 5, 100, 5, 1.0, 0.0)
+    c.views()[2].fill_(float("nan"))
+    c.run()
+    assert np.isfinite(c.gpu_result(np.arange(100))).all()
+    c.check()
+    # alpha = 0: A and B are never read (NaN), C = beta*C
+    c2 = Case(F64, "T", "T", 9, 7, 5, 100, 6, 0.0, 2.0)
+    c2.views()[0].fill_(float("nan"))
+    c2.views()[1].fill_(float("nan"))
+    c2.run()
+    c2.check()
+    # alpha = 0, beta = 0: zeros without reading C
+    c3 = Case(F32, "N", "N", 9, 7, 5, 100, 6, 0.0, 0.0)
+    c3.views()[2].fill_(float("nan"))
+    A, B, C = c3.views()
+    iaat.gemm_strided_batched("N", "N", 9, 7, 5, 0.0, A, c3.lda, c3.sA, B, c3.ldb, c3.sB, 0.0, C, c3.ldc, c3.sC, 100)
+    assert (torch.from_numpy(c3.gpu_result(np.arange(100))) == 0).all()
+    # K = 0: C = beta * C
+    c4 = Case(F32, "N", "N", 9, 7, 0, 50, 8, 1.0, 0.5)
+    c4.run()
+    c4.check()
+
+
+def test_quick_returns_leave_c_untouched():
+    from paper_2208_09822_b200 import iaat
+    c = Case(F32, "N", "N", 8, 8, 8, 10, 5, 0.0, 1.0)
+    before = c.views()[2].clone()
+    n0 = iaat.iaat_launch_count()
+    c.run()  # alpha = 0, beta = 1: no-op, nothing enqueued
+    assert iaat.iaat_launch_count() == n0
+    assert bits_equal(before, c.views()[2])
+    A, B, C = c.views()
+    for M, N, batch in ((0, 8, 10), (8, 0, 10), (8, 8, 0)):
+        st = iaat.gemm_strided_batched("N", "N", M, N, 8, 1.0, A, 8, 64, B, 8, 64, 0.0, C, 8, 64, batch)
+        assert st == 0
+    assert bits_equal(before, c.views()[2])
+
+
+def test_misaligned_bases_and_padding():
+    """Base pointers one element off 16 B, ld padding and problem gaps (NaN
+    sentinels that must never be read), a canary after the last C."""
+    for dtype in (F32, F64):
+        for tr in TRANS:
+            M, N, K = (13, 7, 11) if tr != "TN" else (9, 9, 9)
+            c = Case(dtype, tr[0], tr[1], M, N, K, 333, 12, 1.25, -0.75, pad=3, spad=5, elem_offset=1)
+            C = c.views()[2]
+            tail = C[333 * c.sC:].clone()
+            c.run()
+            c.check()
+            assert bits_equal(tail, C[333 * c.sC:])
+
+
+def test_padding_between_columns_untouched():
+    c = Case(F32, "N", "N", 10, 6, 7, 77, 13, 1.0, 0.0, pad=4)
+    c.run()
+    C = c.views()[2].cpu().numpy()
+    for b in range(77):
+        for j in range(6):
+            s = b * c.sC + j * c.ldc
+            assert np.all(np.isnan(C[s + 10:s + 14]))
+
+
+def test_broadcast_stride_zero():
+    """strideA = 0: every problem uses the same A."""
+    from paper_2208_09822_b200 import iaat
+    import datagen
+    import oracle
+    M, N, K, batch = 12, 20, 16, 500
+    A = datagen.fill_host(21, 0, F32, M, K, M, M * K, [0])
+    B = datagen.fill_host(21, 1, F32, K, N, K, K * N, list(range(batch)))
+    ref, den, _ = oracle.ref_gemm("N", "N", M, N, K, 1.0, A, M, 0, B, K, K * N, 0.0, None, M, M * N, batch)
+    dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    dC = torch.empty(batch * M * N, dtype=torch.float32, device="cuda")
+    iaat.gemm_strided_batched("N", "N", M, N, K, 1.0, dA, M, 0, dB, K, K * N, 0.0, dC, M, M * N, batch)
+    got = dC.view(batch, N, M).double().cpu().numpy()
+    assert oracle.max_rel_err(got, ref, den) <= 1e-5
+
+
+# ---------------------------------------------------------------- pointer-array API
+@pytest.mark.parametrize("dtype", [F32, F64])
+def test_pointer_array_api_shuffled_and_aliased(dtype):
+    from paper_2208_09822_b200 import iaat
+    import oracle
+    rng = np.random.default_rng(3)
+    for tr, (M, N, K) in (("NN", (16, 16, 16)), ("TN", (7, 9, 5)), ("NT", (33, 17, 29)), ("TT", (8, 24, 40))):
+        batch = 257
+        c = Case(dtype, tr[0], tr[1], M, N, K, batch, 31, 1.5, 0.5)
+        A, B, C = c.views()
+        perm = rng.permutation(batch)  # problem b of the call uses storage slot perm[b]
+        esz = A.element_size()
+        Ap = torch.tensor([A.data_ptr() + int(s) * c.sA * esz for s in perm], dtype=torch.int64, device="cuda")
+        Bp = torch.tensor([B.data_ptr() + int(s) * c.sB * esz for s in perm], dtype=torch.int64, device="cuda")
+        Cp = torch.tensor([C.data_ptr() + int(s) * c.sC * esz for s in perm], dtype=torch.int64, device="cuda")
+        iaat.gemm_batched(tr[0], tr[1], M, N, K, 1.5, Ap, c.lda, Bp, c.ldb, 0.5, Cp, c.ldc, batch,
+                          dtype=0 if dtype == F32 else 1)
+        c.check()  # slot s holds problem s's inputs and must hold its result
+    # aliased A and B (same storage): C = A * A^T
+    M = K = 12
+    N = 12
+    c = Case(dtype, "N", "T", M, N, K, 64, 32, 1.0, 0.0)
+    A = c.views()[0]
+    esz = A.element_size()
+    Ap = torch.tensor([A.data_ptr() + b * c.sA * esz for b in range(64)], dtype=torch.int64, device="cuda")
+    C = c.views()[2]
+    Cp = torch.tensor([C.data_ptr() + b * c.sC * esz for b in range(64)], dtype=torch.int64, device="cuda")
+    iaat.gemm_batched("N", "T", M, N, K, 1.0, Ap, c.lda, Ap, c.lda, 0.0, Cp, c.ldc, 64,
+                      dtype=0 if dtype == F32 else 1)
+    Ah = A[:64 * c.sA].double().cpu().numpy()
+    ref, den, _ = oracle.ref_gemm("N", "T", M, N, K, 1.0, Ah, c.lda, c.sA, Ah, c.lda, c.sA, 0.0, None, c.ldc,
+                                  c.sC, 64)
+    got = c.gpu_result(np.arange(64))
+    assert oracle.max_rel_err(got, ref, den) <= TOL[dtype]
+
+
+# ---------------------------------------------------------------- error statuses
+def test_invalid_arguments_enqueue_nothing():
+    from paper_2208_09822_b200 import iaat
+    c = Case(F32, "N", "N", 8, 8, 8, 4, 1, 1.0, 0.0)
+    A, B, C = c.views()
+    before = C.clone()
+    n0 = iaat.iaat_launch_count()
+    f = iaat.iaat_gemm_strided_batched
+    a, b, cc = A.data_ptr(), B.data_ptr(), C.data_ptr()
+    assert f(0, "C", "N", 8, 8, 8, 1.0, a, 8, 64, b, 8, 64, 0.0, cc, 8, 64, 4) == 1
+    assert f(0, "N", "N", -1, 8, 8, 1.0, a, 8, 64, b, 8, 64, 0.0, cc, 8, 64, 4) == 1
+    assert f(0, "N", "N", 8, 8, 8, 1.0, a, 7, 64, b, 8, 64, 0.0, cc, 8, 64, 4) == 1   # lda < M
+    assert f(0, "N", "N", 8, 8, 8, 1.0, a, 8, 64, b, 8, 64, 0.0, cc, 8, 10, 4) == 1   # overlapping C
+    assert f(0, "N", "N", 8, 8, 8, 1.0, a + 2, 8, 64, b, 8, 64, 0.0, cc, 8, 64, 4) == 1  # misaligned
+    assert f(0, "N", "N", 8, 8, 8, 1.0, 0, 8, 64, b, 8, 64, 0.0, cc, 8, 64, 4) == 1   # NULL A
+    assert f(0, "N", "N", 81, 81, 81, 1.0, a, 81, 64, b, 81, 64, 0.0, cc, 81, 6561, 4) == 2
+    assert f(0, "T", "N", 33, 33, 33, 1.0, a, 33, 64, b, 33, 64, 0.0, cc, 33, 1089, 4) == 2
+    assert f(7, "N", "N", 8, 8, 8, 1.0, a, 8, 64, b, 8, 64, 0.0, cc, 8, 64, 4) == 1
+    torch.cuda.synchronize()
+    assert iaat.iaat_launch_count() == n0
+    assert bits_equal(before, C)
+
+
+def test_launch_uses_sm100_kernels_only():
+    """The call enqueues exactly one launch (the persistent plan)."""
+    from paper_2208_09822_b200 import iaat
+    c = Case(F32, "N", "N", 32, 32, 32, 1000, 1, 1.0, 0.0)
+    n0 = iaat.iaat_launch_count()
+    c.run()
+    assert iaat.iaat_launch_count() == n0 + 1
