@@ -8,6 +8,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -70,9 +71,26 @@ Key make_key(const PlanRequest &r)
     return k;
 }
 
+// Tuning knobs (IAAT_FORCE_*) are part of the cache key so that a forced
+// plan is planned once, like any other.
+int64_t forced_key()
+{
+    static const char *names[] = {"IAAT_FORCE_P", "IAAT_FORCE_S", "IAAT_FORCE_TILE", "IAAT_FORCE_FAMILY",
+                                  "IAAT_FORCE_CTAS", "IAAT_FORCE_ORDER"};
+    uint64_t h = 0;
+    for (const char *n : names) {
+        const char *v = std::getenv(n);
+        h = h * 1099511628211ull + 7;
+        if (v)
+            for (const char *q = v; *q; ++q) h = (h ^ (uint64_t)(unsigned char)*q) * 1099511628211ull;
+    }
+    return (int64_t)h;
+}
+
 const Plan &cached_plan(const PlanRequest &r)
 {
     Key k = make_key(r);
+    k.v[18] = forced_key();
     std::lock_guard<std::mutex> lock(g_mu);
     auto it = g_cache.find(k);
     if (it != g_cache.end()) return it->second;

@@ -147,12 +147,13 @@ __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(
 struct StageView {
     unsigned char *a;  // this stage's A region
     unsigned char *b;  // this stage's B region
+    unsigned char *c;  // this stage's C_in region (c_in_smem only)
 };
 
 __device__ __forceinline__ StageView stage_view(const IaatKParams &p, unsigned char *smem, int s)
 {
     unsigned char *base = smem + IAAT_BAR_BYTES + (size_t)s * p.stage_bytes;
-    return StageView{base, base + p.capA};
+    return StageView{base, base + p.capA, base + p.capA + p.capB};
 }
 
 // Global byte address of problem b's operand (strided or pointer-array API).
@@ -160,6 +161,11 @@ __device__ __forceinline__ const char *prob_ptr(const char *base, const void *co
                                                 int64_t stride_bytes, int64_t b)
 {
     return arr ? reinterpret_cast<const char *>(arr[b]) : base + b * stride_bytes;
+}
+
+__device__ __forceinline__ const void *const *cptrs(const IaatKParams &p)
+{
+    return reinterpret_cast<const void *const *>(p.Carr);
 }
 
 // Byte offset, inside the stage region, of local problem pl's operand.
@@ -220,10 +226,14 @@ __device__ void producer_loop(const IaatKParams &p, unsigned char *smem, uint64_
         const int np = (int)min((int64_t)p.P, p.batch - b0);
         StageView sv = stage_view(p, smem, s);
         // pass 1: count bytes, arm the barrier; pass 2: issue the copies
+        const void *const *carr = reinterpret_cast<const void *const *>(p.Carr);
         unsigned bytes = stage_operand<T>(false, p.modeA, p.A, p.Aarr, p.sA, p.spanA, p.slotA,
                                           b0, np, sv.a, &full[s], pol, lane) +
                          stage_operand<T>(false, p.modeB, p.B, p.Barr, p.sB, p.spanB, p.slotB,
                                           b0, np, sv.b, &full[s], pol, lane);
+        if (p.c_in_smem)
+            bytes += stage_operand<T>(false, p.modeC, p.C, carr, p.sC, p.spanC, p.slotC, b0, np,
+                                      sv.c, &full[s], pol, lane);
         bytes = warp_sum(bytes);
         if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes);
         __syncwarp();
@@ -231,6 +241,9 @@ __device__ void producer_loop(const IaatKParams &p, unsigned char *smem, uint64_
                          &full[s], pol, lane);
         stage_operand<T>(true, p.modeB, p.B, p.Barr, p.sB, p.spanB, p.slotB, b0, np, sv.b,
                          &full[s], pol, lane);
+        if (p.c_in_smem)
+            stage_operand<T>(true, p.modeC, p.C, carr, p.sC, p.spanC, p.slotC, b0, np, sv.c,
+                             &full[s], pol, lane);
         if (p.prefetch_c) {
             // C_in will be read by the epilogue: warm L2 now (no smem needed)
             const int64_t scb = p.sC * (int64_t)sizeof(T);
@@ -350,14 +363,16 @@ __device__ __forceinline__ void fma_tile(T (&acc)[MR][NR], const T *__restrict__
 }
 
 // C = alpha*acc + beta*C_in, written once per element, never past the tile.
+// Cin: where C_in is read (the staged smem copy, or C itself); same ldc.
 template <typename T, int MR, int NR, bool VEC>
-__device__ __forceinline__ void epilogue(T (&acc)[MR][NR], T *C, int ldc, int row0, int col0,
-                                         T alpha, T beta, bool beta_zero)
+__device__ __forceinline__ void epilogue(T (&acc)[MR][NR], T *C, const T *Cin, int ldc, int row0,
+                                         int col0, T alpha, T beta, bool beta_zero)
 {
     constexpr int W = VecOf<T>::W;
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
         T *c = C + row0 + (int64_t)(col0 + j) * ldc;
+        const T *ci_p = Cin + row0 + (int64_t)(col0 + j) * ldc;
         if (VEC && (MR % W) == 0) {
 #pragma unroll
             for (int q = 0; q < MR / W; ++q) {
@@ -367,7 +382,7 @@ __device__ __forceinline__ void epilogue(T (&acc)[MR][NR], T *C, int ldc, int ro
                     for (int w = 0; w < W; ++w) o[w] = mul_rn(alpha, acc[q * W + w][j]);
                 } else {
                     T ci[W];
-                    ld_vec<T>(c + q * W, ci);
+                    ld_vec<T>(ci_p + q * W, ci);
 #pragma unroll
                     for (int w = 0; w < W; ++w) o[w] = fma_rn(alpha, acc[q * W + w][j], mul_rn(beta, ci[w]));
                 }
@@ -376,7 +391,7 @@ __device__ __forceinline__ void epilogue(T (&acc)[MR][NR], T *C, int ldc, int ro
         } else {
 #pragma unroll
             for (int i = 0; i < MR; ++i) {
-                T o = beta_zero ? mul_rn(alpha, acc[i][j]) : fma_rn(alpha, acc[i][j], mul_rn(beta, c[i]));
+                T o = beta_zero ? mul_rn(alpha, acc[i][j]) : fma_rn(alpha, acc[i][j], mul_rn(beta, ci_p[i]));
                 c[i] = o;
             }
         }
@@ -392,7 +407,9 @@ __device__ __forceinline__ void fma_class_loop(const IaatKParams &p, const IaatC
     const int idx = (warp - c.warp_begin) * 32 + lane;
     const int pl = idx / c.tiles;  // local problem of this lane
     const int t = idx - pl * c.tiles;
-    const int ti = t % c.tm, tj = t / c.tm;
+    // lanes vary fastest along the tile-contiguous operand (broadcast on the other)
+    const int ti = c.colfast ? t / c.tn : t % c.tm;
+    const int tj = c.colfast ? t % c.tn : t / c.tm;
     const int row0 = c.row_base + ti * MR, col0 = c.col_base + tj * NR;
     const T alpha = (T)p.alpha, beta = (T)p.beta;
     const int64_t sab = p.sA * (int64_t)sizeof(T), sbb = p.sB * (int64_t)sizeof(T);
@@ -421,12 +438,25 @@ __device__ __forceinline__ void fma_class_loop(const IaatKParams &p, const IaatC
                 sv.b + smem_offset(p.modeB, b_first, b_prob, sbb, p.slotB, pl));
             fma_tile<T, TA, TB, MR, NR, VEC>(acc, sA, sB, p.lda, p.ldb, p.K, row0, col0);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);  // stage s no longer read by this warp
+        if (!p.c_in_smem) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);  // stage s no longer read by this warp
+        }
         if (active) {
-            T *C = p.Carr ? reinterpret_cast<T *>(p.Carr[b0 + pl])
-                          : reinterpret_cast<T *>(p.C + (b0 + pl) * scb);
-            epilogue<T, MR, NR, VEC>(acc, C, p.ldc, row0, col0, alpha, beta, p.beta_zero != 0);
+            const char *c_first = prob_ptr(p.C, cptrs(p), scb, b0);
+            const char *c_prob = prob_ptr(p.C, cptrs(p), scb, b0 + pl);
+            T *C = const_cast<T *>(reinterpret_cast<const T *>(c_prob));
+            const T *Cin = C;
+            if (p.c_in_smem) {
+                StageView sv = stage_view(p, smem, s);
+                Cin = reinterpret_cast<const T *>(
+                    sv.c + smem_offset(p.modeC, c_first, c_prob, scb, p.slotC, pl));
+            }
+            epilogue<T, MR, NR, VEC>(acc, C, Cin, p.ldc, row0, col0, alpha, beta, p.beta_zero != 0);
+        }
+        if (p.c_in_smem) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);  // stage s (incl. C_in) no longer read
         }
     }
 }

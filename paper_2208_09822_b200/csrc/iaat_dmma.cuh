@@ -103,7 +103,8 @@ __device__ __forceinline__ void dmma_class_loop(const IaatKParams &p, const Iaat
         const int items = np * c.tiles;
         for (int item = wi; item < items; item += nw) {
             const int pl = item / c.tiles, tt = item - pl * c.tiles;
-            const int ti = tt % c.tm, tj = tt / c.tm;
+            const int ti = c.colfast ? tt / c.tn : tt % c.tm;
+            const int tj = c.colfast ? tt % c.tn : tt / c.tm;
             const int row0 = c.row_base + ti * 8 * WM, col0 = c.col_base + tj * 8 * WN;
             const char *a_prob = p.modeA == IAAT_STAGE_SLAB ? a_first : prob_ptr(p.A, p.Aarr, sab, b0 + pl);
             const char *b_prob = p.modeB == IAAT_STAGE_SLAB ? b_first : prob_ptr(p.B, p.Barr, sbb, b0 + pl);
@@ -117,13 +118,20 @@ __device__ __forceinline__ void dmma_class_loop(const IaatKParams &p, const Iaat
 #pragma unroll
                 for (int nj = 0; nj < WN; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
             dmma_tile<TA, TB, WM, WN>(acc, sA, sB, p.lda, p.ldb, p.K, row0, col0, g, t);
-            double *C = p.Carr ? reinterpret_cast<double *>(p.Carr[b0 + pl])
-                               : reinterpret_cast<double *>(p.C + (b0 + pl) * scb);
+            const char *c_first = prob_ptr(p.C, cptrs(p), scb, b0);
+            const char *c_prob = prob_ptr(p.C, cptrs(p), scb, b0 + pl);
+            double *C = const_cast<double *>(reinterpret_cast<const double *>(c_prob));
+            const double *Cin = C;
+            if (p.c_in_smem)
+                Cin = reinterpret_cast<const double *>(
+                    sv.c + smem_offset(p.modeC, c_first, c_prob, scb, p.slotC, pl));
 #pragma unroll
             for (int mi = 0; mi < WM; ++mi)
 #pragma unroll
                 for (int nj = 0; nj < WN; ++nj) {
-                    double *cp = C + (row0 + 8 * mi + 2 * t) + (int64_t)(col0 + 8 * nj + g) * p.ldc;
+                    const int64_t eo = (row0 + 8 * mi + 2 * t) + (int64_t)(col0 + 8 * nj + g) * p.ldc;
+                    double *cp = C + eo;
+                    const double *cip = Cin + eo;
                     double o[2];
                     if (VEC) {
                         if (p.beta_zero) {
@@ -131,7 +139,7 @@ __device__ __forceinline__ void dmma_class_loop(const IaatKParams &p, const Iaat
                             o[1] = mul_rn(alpha, acc[mi][nj][1]);
                         } else {
                             double ci[2];
-                            ld_vec<double>(cp, ci);
+                            ld_vec<double>(cip, ci);
                             o[0] = fma_rn(alpha, acc[mi][nj][0], mul_rn(beta, ci[0]));
                             o[1] = fma_rn(alpha, acc[mi][nj][1], mul_rn(beta, ci[1]));
                         }
@@ -140,7 +148,7 @@ __device__ __forceinline__ void dmma_class_loop(const IaatKParams &p, const Iaat
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
                             cp[h] = p.beta_zero ? mul_rn(alpha, acc[mi][nj][h])
-                                                : fma_rn(alpha, acc[mi][nj][h], mul_rn(beta, cp[h]));
+                                                : fma_rn(alpha, acc[mi][nj][h], mul_rn(beta, cip[h]));
                     }
                 }
         }

@@ -38,7 +38,8 @@ struct IaatClass {
     int mr;          // tile rows (== the catalog entry's MR; kept for host printing)
     int col_base;    // first column of the class' column strip
     int nr;          // tile columns
-    int units;       // lanes (FMA family) or warps (DMMA family) per problem
+    int tn;          // tiles along N inside the class
+    int colfast;     // lane/tile order: 0 = row tiles fastest, 1 = column tiles fastest
 };
 
 struct IaatKParams {
@@ -58,13 +59,14 @@ struct IaatKParams {
     int P;               // problems per group (one pipeline stage)
     int S;               // pipeline stages
     int n_compute_warps;
-    int modeA, modeB;    // IaatStage
-    int spanA, spanB;    // bytes spanned by one problem's A / B
-    int slotA, slotB;    // per-problem smem slot (PERPROB mode), bytes
-    int capA, capB;      // smem bytes reserved per stage for A / B (multiple of 128)
-    int stage_bytes;     // capA + capB
-    int beta_zero;       // 1: C is write-only
-    int prefetch_c;      // 1: producer prefetches the C span into L2
+    int modeA, modeB, modeC;  // IaatStage
+    int spanA, spanB, spanC;  // bytes spanned by one problem's A / B / C
+    int slotA, slotB, slotC;  // per-problem smem slot (PERPROB mode), bytes
+    int capA, capB, capC;     // smem bytes reserved per stage (multiples of 128); capC = 0: C_in not staged
+    int stage_bytes;          // capA + capB + capC
+    int beta_zero;            // 1: C is write-only
+    int c_in_smem;            // 1: C_in staged with A/B (beta != 0); 0 and beta != 0: read from global
+    int prefetch_c;           // 1: producer prefetches the C span into L2 (when C_in is read from global)
     int nclasses;
     IaatClass cls[IAAT_MAX_CLASSES];
 };

@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -105,7 +106,7 @@ std::vector<DimSplit> splits(int D, int maxt, int vw)
 }
 
 struct Geo {
-    int64_t spanA, spanB;  // bytes of one problem's operand span
+    int64_t spanA, spanB, spanC;  // bytes of one problem's operand span
     int elt;
 };
 
@@ -115,11 +116,11 @@ struct Candidate {
     double group = 0;
     int64_t memops = 0;
     int area = 0;
-    int P = 0, S = 0, W = 0;
+    int P = 0, S = 0, W = 0, ctas = 1;
     int family = IAAT_FAM_FMA;
     DimSplit ms, ns;
-    int wm = 1, wn = 1;  // DMMA warp tile (in 8x8 blocks)
-    int capA = 0, capB = 0, slotA = 0, slotB = 0, modeA = 0, modeB = 0;
+    int capA = 0, capB = 0, capC = 0, slotA = 0, slotB = 0, slotC = 0, modeA = 0, modeB = 0, modeC = 0;
+    int c_in_smem = 0;
     IaatClass cls[IAAT_MAX_CLASSES];
     int ncls = 0;
 };
@@ -149,18 +150,108 @@ bool better(const Candidate &a, const Candidate &b)
     return a.area > b.area;
 }
 
-// Thread instructions of one FMA tile over the whole K (model).
-double fma_tile_instr(const PlanRequest &r, bool vec, int mr, int nr, int vw)
+// ---------------------------------------------------------------- smem model
+// Shared-memory wavefronts of one warp-wide load: lanes request `width`
+// bytes at byte offsets addr[l]; 32 banks x 4 B; identical words broadcast.
+// wavefronts = max over banks of the distinct words that bank must serve.
+int wavefronts(const int64_t *addr, int width, int nl)
 {
-    const bool a_kc = r.transA == 1, b_kc = r.transB == 0;
-    auto loads = [&](bool kcontig, int d) -> double {
-        if (!vec) return d;
-        if (kcontig) return (double)d / vw;  // one vector per row per vw k-steps
-        return d % vw == 0 ? (double)d / vw : d;
+    int64_t words[32][64];
+    int cnt[32] = {0};
+    int worst = 1;
+    for (int l = 0; l < nl; ++l) {
+        for (int w = 0; w < width / 4; ++w) {
+            const int64_t word = addr[l] / 4 + w;
+            const int b = (int)(word & 31);
+            bool seen = false;
+            for (int q = 0; q < cnt[b]; ++q)
+                if (words[b][q] == word) {
+                    seen = true;
+                    break;
+                }
+            if (!seen && cnt[b] < 64) {
+                words[b][cnt[b]++] = word;
+                worst = std::max(worst, cnt[b]);
+            }
+        }
+    }
+    return worst;
+}
+
+struct ClassCost {
+    double instr = 0;   // warp instructions of one tile pass (whole K + epilogue)
+    double wf = 0;      // smem wavefronts of one tile pass
+    double single = 0;  // latency-bound duration of one warp's tile pass (cycles)
+};
+
+// Cost of one warp of an FMA class: simulate the lane -> (problem, tile)
+// mapping of iaat_device.cuh for the first warp and count load instructions
+// and their smem wavefronts for one KU k-block, then scale to K.
+ClassCost fma_class_cost(const PlanRequest &r, bool vec, int elt, int mr, int nr, int tiles, int tm, int tn,
+                         int row_base, int col_base, int colfast, int64_t pstrideA, int64_t pstrideB,
+                         int64_t pstrideC)
+{
+    const int VW = 16 / elt, KU = VW;
+    const bool TA = r.transA == 1, TB = r.transB == 1;
+    int64_t offA[32], offB[32], offC[32];
+    int row0[32], col0[32];
+    for (int l = 0; l < 32; ++l) {
+        const int pl = l / tiles, t = l % tiles;
+        const int ti = colfast ? t / tn : t % tm, tj = colfast ? t % tn : t / tm;
+        row0[l] = row_base + ti * mr;
+        col0[l] = col_base + tj * nr;
+        offA[l] = pl * pstrideA;
+        offB[l] = pl * pstrideB;
+        offC[l] = pl * pstrideC;
+    }
+    int64_t ad[32];
+    double ninstr = 0, nwf = 0;
+    // one KU block of op(A): tile-contiguous unless TA
+    auto operand = [&](bool kcontig, int R, const int *r0, const int64_t *off, int64_t ld) {
+        if (!kcontig) {
+            const bool v = vec && R % VW == 0;
+            for (int kk = 0; kk < KU; ++kk) {
+                const int nld = v ? R / VW : R;
+                for (int q = 0; q < nld; ++q) {
+                    for (int l = 0; l < 32; ++l)
+                        ad[l] = off[l] + (int64_t)(r0[l] + (v ? q * VW : q) + kk * ld) * elt;
+                    ninstr += 1;
+                    nwf += wavefronts(ad, v ? 16 : elt, 32);
+                }
+            }
+        } else {
+            for (int i = 0; i < R; ++i) {
+                const int nld = vec ? 1 : KU;
+                for (int q = 0; q < nld; ++q) {
+                    for (int l = 0; l < 32; ++l) ad[l] = off[l] + (int64_t)(q + (r0[l] + i) * ld) * elt;
+                    ninstr += 1;
+                    nwf += wavefronts(ad, vec ? 16 : elt, 32);
+                }
+            }
+        }
     };
-    const double per_k = mr * nr + loads(a_kc, mr) + loads(b_kc, nr) + 0.5;
-    const double epi = mr * nr * (r.beta_zero ? 2.0 : 4.0);
-    return r.K * per_k + epi + 40.0;
+    operand(TA, mr, row0, offA, r.lda);
+    operand(!TB, nr, col0, offB, r.ldb);
+    const double nblocks = (double)r.K / KU;
+    ClassCost c;
+    c.instr = nblocks * (ninstr + (double)KU * mr * nr + 2);
+    c.wf = nblocks * nwf;
+    // epilogue: C_in smem loads (beta != 0), FMUL/FFMA, global stores
+    const bool vc = vec && mr % VW == 0;
+    if (!r.beta_zero) {
+        double wf = 0;
+        for (int j = 0; j < nr; ++j)
+            for (int q = 0; q < (vc ? mr / VW : mr); ++q) {
+                for (int l = 0; l < 32; ++l)
+                    ad[l] = offC[l] + (int64_t)(row0[l] + (vc ? q * VW : q) + (col0[l] + j) * r.ldc) * elt;
+                wf += wavefronts(ad, vc ? 16 : elt, 32);
+            }
+        c.wf += wf;
+        c.instr += nr * (vc ? mr / VW : mr);
+    }
+    c.instr += mr * nr * (r.beta_zero ? 1 : 2) + nr * (vc ? mr / VW : mr) + 60;
+    c.single = c.instr + nblocks * 30.0 + 200.0;
+    return c;
 }
 
 }  // namespace
@@ -180,6 +271,16 @@ int catalog_code(int family, int mr, int nr)
 
 const char *catalog_json() { return kCatalogJson; }
 
+// SM model constants (cycles at ~1.9 GHz), calibrated on B200 sweeps
+// (tools/sweep.py; profiles/ round 1).
+constexpr double kLoadLatency = 2200.0;   // issue -> full for a bulk-copied stage (besides size/BW)
+constexpr double kIssuePerClk = 4.0;      // warp instructions per SM per clock (4 SMSPs)
+constexpr double kIssuePerWarp = 0.45;    // sustained issue of one warp (LDS/FMA latency, MIO)
+constexpr double kSmemPerClk = 1.0;       // smem wavefronts per SM per clock
+constexpr double kGroupFixed = 500.0;     // per-group barrier / dispatch / epilogue tail
+constexpr double kGlobalCinPenalty = 1500.0;  // exposed L2/HBM latency of C_in read in the epilogue
+constexpr double kOverlapLoss = 0.3;      // fraction of the shorter of (memory, compute) not hidden
+
 Plan make_plan(const PlanRequest &r)
 {
     Plan plan;
@@ -194,6 +295,7 @@ Plan make_plan(const PlanRequest &r)
     const int64_t colsB = r.transB ? K : N, rowsB = r.transB ? N : K;
     geo.spanA = ((colsA - 1) * r.lda + rowsA) * elt;
     geo.spanB = ((colsB - 1) * r.ldb + rowsB) * elt;
+    geo.spanC = ((N - 1) * r.ldc + M) * elt;
 
     // 16-byte vector paths are legal iff every problem's A, B, C base and
     // every column start is 16 B aligned (strided API only).
@@ -202,31 +304,69 @@ Plan make_plan(const PlanRequest &r)
                      (r.batch <= 1 || (al16(r.sA) && al16(r.sB) && al16(r.sC)));
     plan.vec = vec ? 1 : 0;
 
-    const double hbm_per_problem =
-        (double)(M * K + K * N + M * N * (r.beta_zero ? 1 : 2)) * elt;
-    const int64_t sAb = r.sA * elt, sBb = r.sB * elt;
-    const int smem_avail = IAAT_SMEM_LIMIT - IAAT_BAR_BYTES;
+    const double hbm_per_problem = (double)(M * K + K * N + M * N * (r.beta_zero ? 1 : 2)) * elt;
+    const int64_t sAb = r.sA * elt, sBb = r.sB * elt, sCb = r.sC * elt;
+
+    // Test/tuning knobs (never needed in production): force P, S, CTAs/SM,
+    // the first strip sizes or the family, e.g. IAAT_FORCE_P=4 IAAT_FORCE_TILE=8x8.
+    auto envi = [](const char *n) { const char *v = std::getenv(n); return v ? std::atoi(v) : 0; };
+    const int force_p = envi("IAAT_FORCE_P"), force_s = envi("IAAT_FORCE_S"), force_c = envi("IAAT_FORCE_CTAS");
+    int force_mr = 0, force_nr = 0;
+    if (const char *ft = std::getenv("IAAT_FORCE_TILE")) std::sscanf(ft, "%dx%d", &force_mr, &force_nr);
+    const int force_fam = std::getenv("IAAT_FORCE_FAMILY") ? envi("IAAT_FORCE_FAMILY") : -1;
+    const int force_order = std::getenv("IAAT_FORCE_ORDER") ? envi("IAAT_FORCE_ORDER") : -1;
 
     Candidate best;
+    const int64_t pmax_batch = std::max<int64_t>(1, (r.batch + r.sm_count - 1) / r.sm_count);
 
-    auto finish_candidate = [&](Candidate &c, double issue_per_group, double pipe_per_group, int P) {
-        // smem / stages
+    // Evaluate one (tiling, P, CTAs/SM) point.  `warp_instr`, `warp_wf`,
+    // `single`: per-group totals of the compute warps (see ClassCost).
+    auto evaluate = [&](Candidate &c, int P, int ctas, double warp_instr, double warp_wf, double single,
+                        double pipe) -> bool {
+        const int smem_cta = (int)std::min<int64_t>(IAAT_SMEM_LIMIT, 228 * 1024 / ctas - 1024) - IAAT_BAR_BYTES;
         stage_layout(geo.spanA, sAb, P, r.ptr_array, c.modeA, c.slotA, c.capA);
         stage_layout(geo.spanB, sBb, P, r.ptr_array, c.modeB, c.slotB, c.capB);
-        const int64_t stage = (int64_t)c.capA + c.capB;
-        int S = (int)std::min<int64_t>(4, smem_avail / stage);
-        if (S < 1) return false;
-        if (S < 2 && P > 1) return false;
+        c.capC = 0;
+        c.c_in_smem = 0;
+        if (!r.beta_zero) {  // C_in rides in the stage with A and B (read from smem in the epilogue)
+            stage_layout(geo.spanC, sCb, P, r.ptr_array, c.modeC, c.slotC, c.capC);
+            c.c_in_smem = 1;
+        }
+        int64_t stage = (int64_t)c.capA + c.capB + c.capC;
+        int S = (int)std::min<int64_t>(4, smem_cta / stage);
+        if (c.c_in_smem && (S < 1 || (S < 2 && P > 1))) {
+            c.capC = 0;  // C_in does not fit: L2-prefetched C_in read from global
+            c.c_in_smem = 0;
+            stage = (int64_t)c.capA + c.capB;
+            S = (int)std::min<int64_t>(4, smem_cta / stage);
+        }
+        if (force_s > 0) S = (int)std::min<int64_t>(force_s, smem_cta / stage);
+        if (S < 1 || (S < 2 && P > 1)) return false;
         c.S = S;
         c.P = P;
-        const double mem = hbm_per_problem * P / kHbmBytesPerClk;
-        double grp = std::max(mem, std::max(issue_per_group, pipe_per_group)) + kGroupOverhead;
-        if (S == 1) grp = mem + std::max(issue_per_group, pipe_per_group) + kGroupOverhead;
+        c.ctas = ctas;
+        // one "round" = every resident CTA of the SM processes one group
+        const double bytes = ctas * P * hbm_per_problem;
+        const double t_hbm = bytes / kHbmBytesPerClk;
+        const double rate = std::min(kIssuePerClk, kIssuePerWarp * ctas * c.W);
+        const double t_issue = ctas * warp_instr / rate;
+        const double t_smem = ctas * warp_wf / kSmemPerClk;
+        const double t_pipe = ctas * pipe;
+        // a stage is refilled only after its group is consumed: S-1 stages
+        // must cover the load latency of a stage of this size
+        const double t_load = (kLoadLatency + ctas * stage / kHbmBytesPerClk) / (S > 1 ? S - 1 : 1);
+        // compute and staging overlap only partly (the whole CTA moves from
+        // group to group together): T = max(...) + 0.3 * the overlapped part
+        const double t_comp = std::max(std::max(t_issue, t_smem), std::max(t_pipe, single));
+        const double t_mem = std::max(t_hbm, t_load);
+        double t = std::max(t_mem, t_comp) + kOverlapLoss * std::min(t_hbm, t_comp) + kGroupFixed;
+        if (S == 1) t = t_hbm + t_comp + kGroupFixed + kLoadLatency;
+        if (!r.beta_zero && !c.c_in_smem) t += kGlobalCinPenalty;  // C_in latency in the epilogue
         const int64_t ngroups = (r.batch + P - 1) / P;
-        const int64_t grid = std::min<int64_t>(ngroups, r.sm_count);
-        const int64_t waves = (ngroups + grid - 1) / grid;
-        c.group = grp;
-        c.total = grp * (double)waves + 2000.0;  // + launch / pipeline fill
+        const int64_t slots = (int64_t)r.sm_count * ctas;
+        const int64_t waves = (ngroups + slots - 1) / slots;
+        c.group = t;
+        c.total = t * (double)waves + 3000.0;  // launch + pipeline fill/drain
         c.ok = true;
         return true;
     };
@@ -235,108 +375,136 @@ Plan make_plan(const PlanRequest &r)
     const int maxt = 8;
     auto msplits = splits((int)M, maxt, vw);
     auto nsplits = splits((int)N, maxt, vw);
+    const int64_t pstrideA = r.ptr_array ? 0 : sAb, pstrideB = r.ptr_array ? 0 : sBb;
+    const int64_t pstrideC = r.ptr_array ? 0 : sCb;
     for (const auto &ms : msplits) {
         for (const auto &ns : nsplits) {
-            // classes and catalog availability
+            if (force_fam >= 0 && force_fam != IAAT_FAM_FMA) continue;
+            if (force_mr && (ms.s[0].size != force_mr || ns.s[0].size != force_nr)) continue;
             bool avail = true;
             int64_t memops = 2 * M * N;
             int area = 0;
-            struct C4 { int mr, nr, tiles, tm, rb, cb; double instr; } cl[4];
+            struct C4 { int mr, nr, tiles, tm, tn, rb, cb, order; ClassCost cost; } cl[4];
             int ncl = 0;
             int rb = 0;
-            for (int a = 0; a < ms.n; ++a) {
+            for (int a = 0; a < ms.n && avail; ++a) {
                 int cb = 0;
                 for (int b = 0; b < ns.n; ++b) {
                     const int mr = ms.s[a].size, nr = ns.s[b].size;
-                    if (!catalog_has(r.dtype, tidx, IAAT_FAM_FMA, mr, nr)) avail = false;
-                    const int tiles = ms.s[a].count * ns.s[b].count;
-                    cl[ncl++] = {mr, nr, tiles, ms.s[a].count, rb, cb,
-                                 fma_tile_instr(r, vec, mr, nr, vw)};
-                    memops += (int64_t)tiles * (mr + nr) * K;
+                    if (!catalog_has(r.dtype, tidx, IAAT_FAM_FMA, mr, nr)) {
+                        avail = false;
+                        break;
+                    }
+                    const int tm = ms.s[a].count, tn = ns.s[b].count;
+                    C4 q{mr, nr, tm * tn, tm, tn, rb, cb, 0, {}};
+                    // lane order: the cheaper of row-fastest / column-fastest
+                    double bestc = 1e300;
+                    for (int order = 0; order < 2; ++order) {
+                        if (force_order >= 0 && order != force_order) continue;
+                        ClassCost cc = fma_class_cost(r, vec, elt, mr, nr, tm * tn, tm, tn, rb, cb, order,
+                                                      pstrideA, pstrideB, pstrideC);
+                        const double key = std::max(cc.instr / kIssuePerClk, cc.wf);
+                        if (key < bestc * 0.999) {
+                            bestc = key;
+                            q.order = order;
+                            q.cost = cc;
+                        }
+                    }
+                    cl[ncl++] = q;
+                    memops += (int64_t)tm * tn * (mr + nr) * K;
                     area = std::max(area, mr * nr);
                     cb += ns.s[b].size * ns.s[b].count;
                 }
                 rb += ms.s[a].size * ms.s[a].count;
             }
             if (!avail) continue;
-            const int tiles_pp = ms.tiles() * ns.tiles();
-            const int64_t pmax_batch = std::max<int64_t>(1, (r.batch + r.sm_count - 1) / r.sm_count);
-            for (int P = 1; P <= 512; ++P) {
-                if (P > pmax_batch && P > 1) break;
-                int W = 0;
-                double issue = 0;
-                for (int q = 0; q < ncl; ++q) {
-                    const int w = (P * cl[q].tiles + 31) / 32;
-                    W += w;
-                    issue += w * cl[q].instr;
+            for (int ctas = 1; ctas <= 2; ++ctas) {
+                if (force_c && ctas != force_c) continue;
+                const int wmax = IAAT_MAX_THREADS / 32 / ctas - 1;
+                for (int P = 1; P <= 1024; ++P) {
+                    if (P > pmax_batch && P > 1) break;
+                    if (force_p && P != force_p) continue;
+                    int W = 0;
+                    double instr = 0, wf = 0, single = 0;
+                    for (int q = 0; q < ncl; ++q) {
+                        const int w = (P * cl[q].tiles + 31) / 32;
+                        W += w;
+                        instr += w * cl[q].cost.instr;
+                        wf += w * cl[q].cost.wf;
+                        single = std::max(single, cl[q].cost.single);
+                    }
+                    if (W > wmax) break;
+                    double pipe = 0;
+                    if (r.dtype == 1) pipe = (double)P * M * N * K / kDfmaPerClk;
+                    Candidate c;
+                    c.family = IAAT_FAM_FMA;
+                    c.ms = ms;
+                    c.ns = ns;
+                    c.memops = memops;
+                    c.area = area;
+                    c.W = W;
+                    if (!evaluate(c, P, ctas, instr, wf, single, pipe)) continue;
+                    if (!better(c, best)) continue;
+                    int wb = 0;
+                    c.ncls = ncl;
+                    for (int q = 0; q < ncl; ++q) {
+                        const int w = (P * cl[q].tiles + 31) / 32;
+                        c.cls[q] = IaatClass{catalog_code(IAAT_FAM_FMA, cl[q].mr, cl[q].nr), wb, wb + w,
+                                             cl[q].tiles, cl[q].tm, cl[q].rb, cl[q].mr, cl[q].cb, cl[q].nr,
+                                             cl[q].tn, cl[q].order};
+                        wb += w;
+                    }
+                    best = c;
                 }
-                if (W > IAAT_MAX_COMPUTE_WARPS) break;
-                (void)tiles_pp;
-                const double rate = std::min(3.5, 0.5 * W);
-                double pipe = 0;
-                if (r.dtype == 1) pipe = (double)P * M * N * K / kDfmaPerClk;
-                Candidate c;
-                c.family = IAAT_FAM_FMA;
-                c.ms = ms;
-                c.ns = ns;
-                c.memops = memops;
-                c.area = area;
-                c.W = W;
-                if (!finish_candidate(c, issue / rate, pipe, P)) continue;
-                // classes
-                int wb = 0;
-                c.ncls = ncl;
-                for (int q = 0; q < ncl; ++q) {
-                    const int w = (P * cl[q].tiles + 31) / 32;
-                    c.cls[q] = IaatClass{catalog_code(IAAT_FAM_FMA, cl[q].mr, cl[q].nr), wb, wb + w,
-                                         cl[q].tiles, cl[q].tm, cl[q].rb, cl[q].mr, cl[q].cb,
-                                         cl[q].nr, cl[q].tiles};
-                    wb += w;
-                }
-                if (better(c, best)) best = c;
             }
         }
     }
 
     // ------------------------------------------------------------ DMMA family (fp64)
-    if (r.dtype == 1 && M % 8 == 0 && N % 8 == 0) {
+    if (r.dtype == 1 && M % 8 == 0 && N % 8 == 0 && !(force_fam >= 0 && force_fam != IAAT_FAM_DMMA)) {
         for (int wm = 1; wm <= 2; ++wm)
             for (int wn = 1; wn <= 2; ++wn) {
                 if ((M / 8) % wm || (N / 8) % wn) continue;
+                if (force_mr && (8 * wm != force_mr || 8 * wn != force_nr)) continue;
                 if (!catalog_has(1, tidx, IAAT_FAM_DMMA, 8 * wm, 8 * wn)) continue;
                 const int tm = (int)(M / (8 * wm)), tn = (int)(N / (8 * wn));
                 const int tiles = tm * tn;
                 const int64_t memops = (int64_t)tiles * (8 * wm + 8 * wn) * K + 2 * M * N;
-                const int64_t pmax_batch = std::max<int64_t>(1, (r.batch + r.sm_count - 1) / r.sm_count);
                 // per item (one warp tile over K): DMMAs + fragment loads + epilogue
                 const double kst = (double)((K + 3) / 4);
                 const double instr_item = kst * (wm * wn + wm + wn + 2) + wm * wn * (r.beta_zero ? 6 : 10) + 30;
-                for (int P = 1; P <= 64; ++P) {
-                    if (P > pmax_batch && P > 1) break;
-                    const int items = P * tiles;
-                    for (int W = 4; W <= IAAT_MAX_COMPUTE_WARPS; W += 1) {
-                        if (W > items && W > 4) break;
-                        const double per_warp_items = std::ceil((double)items / W);
-                        const double issue = per_warp_items * W * instr_item / std::min(3.5, 0.5 * W);
-                        // DMMA pipe: 128 flop / clk / SM at the fp64 peak
-                        const double pipe = (double)P * 2.0 * M * N * K / 128.0 *
-                                            (per_warp_items * W / items);
-                        Candidate c;
-                        c.family = IAAT_FAM_DMMA;
-                        c.ms.s[0] = {8 * wm, tm};
-                        c.ms.n = 1;
-                        c.ns.s[0] = {8 * wn, tn};
-                        c.ns.n = 1;
-                        c.wm = wm;
-                        c.wn = wn;
-                        c.memops = memops;
-                        c.area = 64 * wm * wn;
-                        c.W = W;
-                        if (!finish_candidate(c, issue, pipe, P)) continue;
-                        c.ncls = 1;
-                        c.cls[0] = IaatClass{catalog_code(IAAT_FAM_DMMA, 8 * wm, 8 * wn), 0, W, tiles, tm,
-                                             0, 8 * wm, 0, 8 * wn, tiles};
-                        if (better(c, best)) best = c;
+                const double wf_item = kst * (wm + wn) * 4.0 + wm * wn * (r.beta_zero ? 0 : 2);
+                for (int ctas = 1; ctas <= 2; ++ctas) {
+                    if (force_c && ctas != force_c) continue;
+                    const int wmax = IAAT_MAX_THREADS / 32 / ctas - 1;
+                    for (int P = 1; P <= 64; ++P) {
+                        if (P > pmax_batch && P > 1) break;
+                        if (force_p && P != force_p) continue;
+                        const int items = P * tiles;
+                        for (int W = 2; W <= wmax; ++W) {
+                            if (W > items && W > 2) break;
+                            const double per_warp = std::ceil((double)items / W);
+                            // DMMA pipe: 128 flop / clk / SM at the fp64 peak
+                            const double pipe = (double)P * 2.0 * M * N * K / 128.0 * (per_warp * W / items);
+                            Candidate c;
+                            c.family = IAAT_FAM_DMMA;
+                            c.ms.s[0] = {8 * wm, tm};
+                            c.ms.n = 1;
+                            c.ns.s[0] = {8 * wn, tn};
+                            c.ns.n = 1;
+                            c.memops = memops;
+                            c.area = 64 * wm * wn;
+                            c.W = W;
+                            const double single = per_warp * (instr_item + kst * 20.0) + 400.0;
+                            if (!evaluate(c, P, ctas, per_warp * W * instr_item, per_warp * W * wf_item, single,
+                                          pipe))
+                                continue;
+                            if (!better(c, best)) continue;
+                            c.ncls = 1;
+                            c.cls[0] = IaatClass{catalog_code(IAAT_FAM_DMMA, 8 * wm, 8 * wn), 0, W, tiles, tm,
+                                                 0, 8 * wm, 0, 8 * wn, tn, 0};
+                            best = c;
+                        }
                     }
                 }
             }
@@ -364,19 +532,25 @@ Plan make_plan(const PlanRequest &r)
     kp.n_compute_warps = best.W;
     kp.modeA = best.modeA;
     kp.modeB = best.modeB;
+    kp.modeC = best.modeC;
     kp.spanA = (int)geo.spanA;
     kp.spanB = (int)geo.spanB;
+    kp.spanC = (int)geo.spanC;
     kp.slotA = best.slotA;
     kp.slotB = best.slotB;
+    kp.slotC = best.slotC;
     kp.capA = best.capA;
     kp.capB = best.capB;
-    kp.stage_bytes = best.capA + best.capB;
+    kp.capC = best.capC;
+    kp.stage_bytes = best.capA + best.capB + best.capC;
     kp.beta_zero = r.beta_zero;
-    kp.prefetch_c = r.beta_zero ? 0 : 1;
+    kp.c_in_smem = best.c_in_smem;
+    kp.prefetch_c = (!r.beta_zero && !best.c_in_smem) ? 1 : 0;
     kp.nclasses = best.ncls;
     for (int q = 0; q < best.ncls; ++q) kp.cls[q] = best.cls[q];
     plan.family = best.family;
-    plan.grid = (int)std::min<int64_t>(kp.ngroups, r.sm_count);
+    plan.ctas = best.ctas;
+    plan.grid = (int)std::min<int64_t>(kp.ngroups, (int64_t)r.sm_count * best.ctas);
     plan.block = (best.W + 1) * 32;
     plan.smem = IAAT_BAR_BYTES + best.S * kp.stage_bytes;
     plan.nm = best.ms.n;
@@ -408,12 +582,14 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
         return s;
     }
     const IaatKParams &k = p.kp;
-    add("\"family\": \"%s\", \"vec\": %d, \"P\": %d, \"S\": %d, \"compute_warps\": %d, \"grid\": %d, "
-        "\"block\": %d, \"smem\": %d, \"ngroups\": %lld, ",
-        p.family == IAAT_FAM_DMMA ? "dmma" : "fma", p.vec, k.P, k.S, k.n_compute_warps, p.grid, p.block,
+    add("\"family\": \"%s\", \"vec\": %d, \"P\": %d, \"S\": %d, \"compute_warps\": %d, \"ctas_per_sm\": %d, "
+        "\"grid\": %d, \"block\": %d, \"smem\": %d, \"ngroups\": %lld, ",
+        p.family == IAAT_FAM_DMMA ? "dmma" : "fma", p.vec, k.P, k.S, k.n_compute_warps, p.ctas, p.grid, p.block,
         p.smem, (long long)k.ngroups);
-    add("\"stage_a\": \"%s\", \"stage_b\": \"%s\", \"cap_a\": %d, \"cap_b\": %d, \"prefetch_c\": %d, ",
-        k.modeA ? "perprob" : "slab", k.modeB ? "perprob" : "slab", k.capA, k.capB, k.prefetch_c);
+    add("\"stage_a\": \"%s\", \"stage_b\": \"%s\", \"stage_c\": \"%s\", \"cap_a\": %d, \"cap_b\": %d, "
+        "\"cap_c\": %d, \"c_in_smem\": %d, \"prefetch_c\": %d, ",
+        k.modeA ? "perprob" : "slab", k.modeB ? "perprob" : "slab", k.modeC ? "perprob" : "slab", k.capA, k.capB,
+        k.capC, k.c_in_smem, k.prefetch_c);
     add("\"m_strips\": [");
     for (int i = 0; i < p.nm; ++i) add("%s[%d, %d]", i ? ", " : "", p.mstrip[i].size, p.mstrip[i].count);
     add("], \"n_strips\": [");
@@ -423,9 +599,9 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
     for (int q = 0; q < k.nclasses; ++q) {
         const IaatClass &c = k.cls[q];
         add("%s{\"code\": %d, \"mr\": %d, \"nr\": %d, \"tiles\": %d, \"tm\": %d, \"row_base\": %d, "
-            "\"col_base\": %d, \"warp_begin\": %d, \"warp_end\": %d}",
+            "\"col_base\": %d, \"warp_begin\": %d, \"warp_end\": %d, \"colfast\": %d}",
             q ? ", " : "", c.code, c.mr, c.nr, c.tiles, c.tm, c.row_base, c.col_base, c.warp_begin,
-            c.warp_end);
+            c.warp_end, c.colfast);
     }
     s += "]}";
     return s;

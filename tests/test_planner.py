@@ -1,0 +1,166 @@
+"""Run-time planner (csrc/planner.cpp) through the host-only C ABI entry
+iaat_plan_describe -- CPU only.
+
+Invariants the kernels rely on: every plan's tile classes cover
+the M x N index set exactly once with catalog tiles ("each block
+has the same size as one of the generated kernels"), warps are partitioned
+into contiguous warp-uniform class ranges, vector-capable classes start on a
+vector boundary, shared memory fits, and planning is deterministic.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+from paper_2208_09822_b200 import iaat
+
+CAT = iaat.iaat_catalog_describe()
+TRANS = ["NN", "NT", "TN", "TT"]
+
+
+def catalog_set():
+    s = set()
+    for e in CAT:
+        s.add((e["family"], e["dtype"], e["trans"], e["mr"], e["nr"]))
+    return s
+
+
+CATSET = catalog_set()
+
+
+def plan(dt, tr, M, N, K, batch=10000, beta0=False, align=256, pad=0):
+    ra, ca = (M, K) if tr[0] == "N" else (K, M)
+    rb, cb = (K, N) if tr[1] == "N" else (N, K)
+    lda, ldb, ldc = ra + pad, rb + pad, M + pad
+    return iaat.iaat_plan_describe(dt, tr[0], tr[1], M, N, K, lda, lda * ca, ldb, ldb * cb, ldc, ldc * N, batch,
+                                   beta0, False, align, 148)
+
+
+def check_plan(p, dt, tr, M, N):
+    assert p["status"] == 0, p
+    cover = np.zeros((M, N), dtype=np.int32)
+    dname = "f32" if dt == 0 else "f64"
+    vw = 4 if dt == 0 else 2
+    wprev = 0
+    for c in p["classes"]:
+        fam = p["family"]
+        assert (fam, dname, tr, c["mr"], c["nr"]) in CATSET, c
+        tm = c["tm"]
+        tn = c["tiles"] // tm
+        assert tm * tn == c["tiles"]
+        for ti, tj in itertools.product(range(tm), range(tn)):
+            r0 = c["row_base"] + ti * c["mr"]
+            c0 = c["col_base"] + tj * c["nr"]
+            cover[r0:r0 + c["mr"], c0:c0 + c["nr"]] += 1
+            assert r0 + c["mr"] <= M and c0 + c["nr"] <= N
+        # warp ranges contiguous and ordered
+        assert c["warp_begin"] == wprev and c["warp_end"] > c["warp_begin"]
+        wprev = c["warp_end"]
+        if fam == "fma":
+            assert p["P"] * c["tiles"] <= 32 * (c["warp_end"] - c["warp_begin"])
+            if p["vec"]:
+                if c["mr"] % vw == 0:
+                    assert c["row_base"] % vw == 0
+                if c["nr"] % vw == 0:
+                    assert c["col_base"] % vw == 0
+    assert np.all(cover == 1), "tiles do not cover C exactly once"
+    assert wprev == p["compute_warps"] <= 15
+    assert p["block"] == 32 * (p["compute_warps"] + 1)
+    assert p["smem"] <= 227 * 1024
+    assert 1 <= p["S"] <= 6
+    assert p["grid"] <= 148 * p["ctas_per_sm"]
+
+
+@pytest.mark.parametrize("tr", TRANS)
+@pytest.mark.parametrize("dt", [0, 1])
+def test_exact_cover_small(dt, tr):
+    for M, N in itertools.product(range(1, 21), repeat=2):
+        K = 7
+        if tr == "TN" and M * N * K > 32768:
+            continue
+        check_plan(plan(dt, tr, M, N, K), dt, tr, M, N)
+
+
+@pytest.mark.parametrize("tr", TRANS)
+@pytest.mark.parametrize("dt", [0, 1])
+def test_exact_cover_sampled_large(dt, tr):
+    rng = np.random.default_rng(dt * 4 + TRANS.index(tr))
+    lim = 32768 if tr == "TN" else 512000
+    n = 0
+    while n < 40:
+        M, N, K = (int(x) for x in rng.integers(1, 81, size=3))
+        if M * N * K > lim:
+            continue
+        n += 1
+        for beta0 in (False, True):
+            check_plan(plan(dt, tr, M, N, K, beta0=beta0), dt, tr, M, N)
+
+
+def test_config_shapes_plan():
+    for n in range(4, 81, 4):
+        for tr in ("NN", "NT", "TT"):
+            check_plan(plan(0, tr, n, n, n, batch=(256 << 20) // (12 * n * n)), 0, tr, n, n)
+    for n in (8, 16, 32, 48, 64, 80):
+        for tr in ("NN", "NT"):
+            p = plan(1, tr, n, n, n, batch=2_000_000, beta0=True)
+            check_plan(p, 1, tr, n, n)
+
+
+def test_misaligned_and_padded_plans_disable_vectors():
+    p = plan(0, "NN", 16, 16, 16, align=4)
+    assert p["vec"] == 0
+    p = plan(0, "NN", 16, 16, 16, pad=1)
+    assert p["vec"] == 0
+    p = plan(0, "NN", 16, 16, 16)
+    assert p["vec"] == 1
+
+
+def test_plan_deterministic():
+    a = plan(0, "NT", 37, 53, 23)
+    b = plan(0, "NT", 37, 53, 23)
+    assert a == b
+
+
+def test_small_batch_uses_all_sms():
+    # config 1: 2000 problems -> at least 148 groups when possible
+    p = plan(0, "NN", 16, 16, 16, batch=2000, beta0=True)
+    assert p["P"] <= -(-2000 // 148)
+    assert p["grid"] == p["ngroups"]
+
+
+def test_memops_is_paper_cost():
+    """memops = sum over tiles (m_i + n_i) K + 2MN."""
+    for (M, N, K) in [(15, 15, 15), (64, 64, 64), (7, 80, 3)]:
+        p = plan(0, "NN", M, N, K)
+        s = sum(c["tiles"] * (c["mr"] + c["nr"]) for c in p["classes"])
+        assert p["memops"] == s * K + 2 * M * N
+
+
+def test_catalog_register_budget():
+    """Every catalog entry fits the generator's register budget (accumulators
+    + live fragments, PAPER.md:217-235 register groups) -- the same budget the
+    no-spill build check (tests/test_build.py) verifies."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "generate", os.path.join(os.path.dirname(iaat.__file__), "gen", "generate.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    for e in CAT:
+        if e["family"] == "fma":
+            assert gen.fma_regs(e["dtype"], e["trans"], e["mr"], e["nr"]) <= gen.REG_BUDGET[e["dtype"]]
+            assert 1 <= e["mr"] <= 8 and 1 <= e["nr"] <= 8
+        else:
+            assert e["dtype"] == "f64" and e["mr"] % 8 == 0 and e["nr"] % 8 == 0
+    # every (mr, nr) <= 4 x 4 exists for every dtype/trans: any M, N has an exact cover
+    for dt in ("f32", "f64"):
+        for tr in TRANS:
+            for mr, nr in itertools.product(range(1, 5), repeat=2):
+                assert ("fma", dt, tr, mr, nr) in CATSET
+
+
+def test_not_small_and_invalid():
+    with pytest.raises(iaat.IaatError):
+        plan(0, "NN", 81, 81, 81)
+    with pytest.raises(iaat.IaatError):
+        plan(0, "TN", 33, 33, 33)
