@@ -6,6 +6,7 @@
 // either enqueues sm_100a kernels or returns an error status.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -76,7 +77,7 @@ Key make_key(const PlanRequest &r)
 int64_t forced_key()
 {
     static const char *names[] = {"IAAT_FORCE_P", "IAAT_FORCE_S", "IAAT_FORCE_TILE", "IAAT_FORCE_FAMILY",
-                                  "IAAT_FORCE_CTAS", "IAAT_FORCE_ORDER"};
+                                  "IAAT_FORCE_CTAS", "IAAT_FORCE_ORDER", "IAAT_FORCE_CSMEM"};
     uint64_t h = 0;
     for (const char *n : names) {
         const char *v = std::getenv(n);
@@ -251,7 +252,8 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
     kp.alpha = a;
     kp.beta = b;
     LaunchFn fn = kLaunch[r.dtype][ta * 2 + tb][plan.vec];
-    cudaError_t e = fn(kp, plan.grid, plan.block, plan.smem, s);
+    static const int smem_pad = std::getenv("IAAT_DEBUG_SMEM_PAD") ? std::atoi(std::getenv("IAAT_DEBUG_SMEM_PAD")) : 0;
+    cudaError_t e = fn(kp, plan.grid, plan.block, std::min(plan.smem + smem_pad, IAAT_SMEM_LIMIT), s);
     if (e != cudaSuccess) {
         g_last_cuda_error = (int)e;
         return IAAT_ERROR_CUDA;

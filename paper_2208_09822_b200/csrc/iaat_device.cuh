@@ -330,7 +330,7 @@ __device__ __forceinline__ void load_one(T (&f)[R], const T *X, int ld, int k, i
 }
 
 // acc(i,j) += sum_k opA(row0+i, k) * opB(k, col0+j), k ascending, one FMA each.
-template <typename T, bool TA, bool TB, int MR, int NR, bool VEC>
+template <typename T, bool TA, bool TB, int MR, int NR, bool VEC, int UNR>
 __device__ __forceinline__ void fma_tile(T (&acc)[MR][NR], const T *__restrict__ sA,
                                          const T *__restrict__ sB, int lda, int ldb, int K,
                                          int row0, int col0)
@@ -338,7 +338,10 @@ __device__ __forceinline__ void fma_tile(T (&acc)[MR][NR], const T *__restrict__
     // A: tile-contiguous iff TA == false;  B: tile-contiguous iff TB == true
     constexpr int KU = KUnroll<T>::value;
     int k = 0;
-#pragma unroll 1
+    // UNR = 2: two k-blocks in flight (the paper's ping-pang, PAPER.md:181 --
+    // the next block's fragments load while this block's FMAs issue); the
+    // generator enables it where the doubled fragments fit the register budget.
+#pragma unroll UNR
     for (; k + KU <= K; k += KU) {
         T a[KU][MR], b[KU][NR];
         load_frag<T, TA, MR, VEC>(a, sA, lda, k, row0);
@@ -399,17 +402,34 @@ __device__ __forceinline__ void epilogue(T (&acc)[MR][NR], T *C, const T *Cin, i
 }
 
 // One compute warp running FMA tile class `c` over all groups of this CTA.
-template <typename T, bool TA, bool TB, int MR, int NR, bool VEC>
+template <typename T, bool TA, bool TB, int MR, int NR, bool VEC, int UNR>
 __device__ __forceinline__ void fma_class_loop(const IaatKParams &p, const IaatClass &c,
                                                unsigned char *smem, uint64_t *full,
                                                uint64_t *empty, int warp, int lane)
 {
-    const int idx = (warp - c.warp_begin) * 32 + lane;
-    const int pl = idx / c.tiles;  // local problem of this lane
-    const int t = idx - pl * c.tiles;
-    // lanes vary fastest along the tile-contiguous operand (broadcast on the other)
-    const int ti = c.colfast ? t / c.tn : t % c.tm;
-    const int tj = c.colfast ? t % c.tn : t / c.tm;
+    int pl, ti, tj;
+    bool tile_ok = true;
+    if (c.bm == 0) {
+        // linear: lane index -> (problem, tile); lanes vary fastest along the
+        // tile-contiguous operand (broadcast on the other)
+        const int idx = (warp - c.warp_begin) * 32 + lane;
+        pl = idx / c.tiles;  // local problem of this lane
+        const int t = idx - pl * c.tiles;
+        ti = c.colfast ? t / c.tn : t % c.tm;
+        tj = c.colfast ? t % c.tn : t / c.tm;
+    } else {
+        // blocked: the warp owns a bm x bn block of one problem's tiles, so a
+        // half-warp's 16-byte loads cover few distinct rows AND columns
+        // (shared-memory wavefronts are per half-warp for 128-bit loads)
+        const int bn = 32 / c.bm;
+        const int nbm = (c.tm + c.bm - 1) / c.bm, nbn = (c.tn + bn - 1) / bn;
+        const int wb = warp - c.warp_begin;
+        pl = wb / (nbm * nbn);
+        const int blk = wb - pl * (nbm * nbn);
+        ti = (blk % nbm) * c.bm + lane % c.bm;
+        tj = (blk / nbm) * bn + lane / c.bm;
+        tile_ok = ti < c.tm && tj < c.tn;
+    }
     const int row0 = c.row_base + ti * MR, col0 = c.col_base + tj * NR;
     const T alpha = (T)p.alpha, beta = (T)p.beta;
     const int64_t sab = p.sA * (int64_t)sizeof(T), sbb = p.sB * (int64_t)sizeof(T);
@@ -419,7 +439,7 @@ __device__ __forceinline__ void fma_class_loop(const IaatKParams &p, const IaatC
         const int s = it % p.S;
         const int64_t b0 = g * p.P;
         const int np = (int)min((int64_t)p.P, p.batch - b0);
-        const bool active = pl < np;
+        const bool active = tile_ok && pl < np;
         T acc[MR][NR];
 #pragma unroll
         for (int i = 0; i < MR; ++i)
@@ -436,7 +456,7 @@ __device__ __forceinline__ void fma_class_loop(const IaatKParams &p, const IaatC
                 sv.a + smem_offset(p.modeA, a_first, a_prob, sab, p.slotA, pl));
             const T *sB = reinterpret_cast<const T *>(
                 sv.b + smem_offset(p.modeB, b_first, b_prob, sbb, p.slotB, pl));
-            fma_tile<T, TA, TB, MR, NR, VEC>(acc, sA, sB, p.lda, p.ldb, p.K, row0, col0);
+            fma_tile<T, TA, TB, MR, NR, VEC, UNR>(acc, sA, sB, p.lda, p.ldb, p.K, row0, col0);
         }
         if (!p.c_in_smem) {
             __syncwarp();

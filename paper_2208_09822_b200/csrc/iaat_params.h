@@ -39,7 +39,9 @@ struct IaatClass {
     int col_base;    // first column of the class' column strip
     int nr;          // tile columns
     int tn;          // tiles along N inside the class
-    int colfast;     // lane/tile order: 0 = row tiles fastest, 1 = column tiles fastest
+    int colfast;     // linear lane/tile order: 0 = row tiles fastest, 1 = column tiles fastest
+    int bm;          // 0: linear mapping (a warp may span problems);  >0: blocked mapping --
+                     // each warp owns a bm x (32/bm) block of tiles of ONE problem
 };
 
 struct IaatKParams {

@@ -22,7 +22,12 @@
 // Ties go to fewer memops (the paper's cost), then bigger tiles.
 #include "planner.h"
 
+#include <dlfcn.h>
+
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <string>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -153,13 +158,15 @@ bool better(const Candidate &a, const Candidate &b)
 // ---------------------------------------------------------------- smem model
 // Shared-memory wavefronts of one warp-wide load: lanes request `width`
 // bytes at byte offsets addr[l]; 32 banks x 4 B; identical words broadcast.
-// wavefronts = max over banks of the distinct words that bank must serve.
-int wavefronts(const int64_t *addr, int width, int nl)
+// Measured on B200 (ncu "L1 Wavefronts Shared"): 128-bit loads are served
+// per HALF-warp (each half >= 1 wavefront), narrower loads per warp; inside
+// a group, wavefronts = max over banks of the distinct words that bank serves.
+int wf_group(const int64_t *addr, int width, int l0, int l1)
 {
     int64_t words[32][64];
     int cnt[32] = {0};
     int worst = 1;
-    for (int l = 0; l < nl; ++l) {
+    for (int l = l0; l < l1; ++l) {
         for (int w = 0; w < width / 4; ++w) {
             const int64_t word = addr[l] / 4 + w;
             const int b = (int)(word & 31);
@@ -178,31 +185,75 @@ int wavefronts(const int64_t *addr, int width, int nl)
     return worst;
 }
 
+int wavefronts(const int64_t *addr, int width, int nl)
+{
+    if (width == 16) return wf_group(addr, width, 0, nl / 2) + wf_group(addr, width, nl / 2, nl);
+    return wf_group(addr, width, 0, nl);
+}
+
 struct ClassCost {
     double instr = 0;   // warp instructions of one tile pass (whole K + epilogue)
     double wf = 0;      // smem wavefronts of one tile pass
     double single = 0;  // latency-bound duration of one warp's tile pass (cycles)
 };
 
-// Cost of one warp of an FMA class: simulate the lane -> (problem, tile)
-// mapping of iaat_device.cuh for the first warp and count load instructions
-// and their smem wavefronts for one KU k-block, then scale to K.
-ClassCost fma_class_cost(const PlanRequest &r, bool vec, int elt, int mr, int nr, int tiles, int tm, int tn,
-                         int row_base, int col_base, int colfast, int64_t pstrideA, int64_t pstrideB,
-                         int64_t pstrideC)
+// Lane -> (local problem, tile row, tile col) of the first warp of a class
+// under a mapping (see fma_class_loop): map = -2 linear row-fastest, -1 linear
+// column-fastest, bm > 0 blocked bm x (32/bm).
+struct Lanes {
+    int pl[32], ti[32], tj[32];
+    int active;
+};
+
+Lanes lane_map(int map, int tiles, int tm, int tn)
+{
+    Lanes L;
+    L.active = 0;
+    for (int l = 0; l < 32; ++l) {
+        if (map < 0) {
+            L.pl[l] = l / tiles;
+            const int t = l % tiles;
+            L.ti[l] = map == -1 ? t / tn : t % tm;
+            L.tj[l] = map == -1 ? t % tn : t / tm;
+        } else {
+            L.pl[l] = 0;
+            L.ti[l] = l % map;
+            L.tj[l] = l / map;
+        }
+        const bool ok = L.ti[l] < tm && L.tj[l] < tn;
+        if (!ok) {  // idle lane: park it on tile (0,0) (its loads are not issued)
+            L.ti[l] = 0;
+            L.tj[l] = 0;
+        }
+        L.active += ok;
+    }
+    return L;
+}
+
+// Warps a class needs for P problems under a mapping.
+int class_warps(int map, int P, int tiles, int tm, int tn)
+{
+    if (map < 0) return (P * tiles + 31) / 32;
+    const int bn = 32 / map;
+    return P * ((tm + map - 1) / map) * ((tn + bn - 1) / bn);
+}
+
+// Cost of one warp of an FMA class: simulate the mapping of the first warp
+// and count load instructions and their smem wavefronts for one KU k-block,
+// then scale to K.
+ClassCost fma_class_cost(const PlanRequest &r, bool vec, int elt, int mr, int nr, const Lanes &L, int row_base,
+                         int col_base, int64_t pstrideA, int64_t pstrideB, int64_t pstrideC)
 {
     const int VW = 16 / elt, KU = VW;
     const bool TA = r.transA == 1, TB = r.transB == 1;
     int64_t offA[32], offB[32], offC[32];
     int row0[32], col0[32];
     for (int l = 0; l < 32; ++l) {
-        const int pl = l / tiles, t = l % tiles;
-        const int ti = colfast ? t / tn : t % tm, tj = colfast ? t % tn : t / tm;
-        row0[l] = row_base + ti * mr;
-        col0[l] = col_base + tj * nr;
-        offA[l] = pl * pstrideA;
-        offB[l] = pl * pstrideB;
-        offC[l] = pl * pstrideC;
+        row0[l] = row_base + L.ti[l] * mr;
+        col0[l] = col_base + L.tj[l] * nr;
+        offA[l] = L.pl[l] * pstrideA;
+        offB[l] = L.pl[l] * pstrideB;
+        offC[l] = L.pl[l] * pstrideC;
     }
     int64_t ad[32];
     double ninstr = 0, nwf = 0;
@@ -281,7 +332,96 @@ constexpr double kGroupFixed = 500.0;     // per-group barrier / dispatch / epil
 constexpr double kGlobalCinPenalty = 1500.0;  // exposed L2/HBM latency of C_in read in the epilogue
 constexpr double kOverlapLoss = 0.3;      // fraction of the shorter of (memory, compute) not hidden
 
+struct Knobs {
+    int p = 0, s = 0, ctas = 0, mr = 0, nr = 0, fam = -1, order = -1, csmem = -1;
+    bool any() const { return p || s || ctas || mr || fam >= 0 || order >= 0 || csmem >= 0; }
+};
+
+Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn);
+
+// ---------------------------------------------------------------- install-time tuning table
+// tuning/b200.tsv next to libiaat.so (written by paper_2208_09822_b200/tune.py on
+// a B200: the install-time stage's "automatically tunes kernels based on
+// features of the hardware").  One line per tuned input:
+//   dtype tA tB M N K lda ldb ldc packed beta0 vec : mr nr P S ctas order family [csmem]
+struct TunedKey {
+    int v[12];
+    bool operator<(const TunedKey &o) const { return std::lexicographical_compare(v, v + 12, o.v, o.v + 12); }
+};
+
+const std::map<TunedKey, Knobs> &tuning_table()
+{
+    static std::map<TunedKey, Knobs> table;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        std::string path;
+        if (const char *e = std::getenv("IAAT_TUNING")) {
+            path = e;
+        } else {
+            Dl_info info;
+            if (dladdr((void *)&tuning_table, &info) && info.dli_fname) {
+                path = info.dli_fname;
+                const size_t slash = path.find_last_of('/');
+                path = (slash == std::string::npos ? std::string(".") : path.substr(0, slash)) + "/tuning/b200.tsv";
+            }
+        }
+        FILE *f = path.empty() ? nullptr : std::fopen(path.c_str(), "r");
+        if (!f) return;
+        char line[512];
+        while (std::fgets(line, sizeof line, f)) {
+            if (line[0] == '#') continue;
+            TunedKey k;
+            Knobs kn;
+            int n = std::sscanf(line, "%d %d %d %d %d %d %d %d %d %d %d %d : %d %d %d %d %d %d %d %d", &k.v[0],
+                                &k.v[1], &k.v[2], &k.v[3], &k.v[4], &k.v[5], &k.v[6], &k.v[7], &k.v[8], &k.v[9],
+                                &k.v[10], &k.v[11], &kn.mr, &kn.nr, &kn.p, &kn.s, &kn.ctas, &kn.order, &kn.fam,
+                                &kn.csmem);
+            if (n == 19) kn.csmem = -1;
+            if (n >= 19) table[k] = kn;
+        }
+        std::fclose(f);
+    });
+    return table;
+}
+
 Plan make_plan(const PlanRequest &r)
+{
+    Knobs kn;
+    // Test/tuning knobs (never needed in production): force P, S, CTAs/SM,
+    // the first strip sizes, the lane mapping or the family, e.g.
+    // IAAT_FORCE_P=4 IAAT_FORCE_TILE=8x8.
+    auto envi = [](const char *n) { const char *v = std::getenv(n); return v ? std::atoi(v) : 0; };
+    kn.p = envi("IAAT_FORCE_P");
+    kn.s = envi("IAAT_FORCE_S");
+    kn.ctas = envi("IAAT_FORCE_CTAS");
+    if (const char *ft = std::getenv("IAAT_FORCE_TILE")) std::sscanf(ft, "%dx%d", &kn.mr, &kn.nr);
+    kn.fam = std::getenv("IAAT_FORCE_FAMILY") ? envi("IAAT_FORCE_FAMILY") : -1;
+    kn.order = std::getenv("IAAT_FORCE_ORDER") ? envi("IAAT_FORCE_ORDER") : -1;
+    kn.csmem = std::getenv("IAAT_FORCE_CSMEM") ? envi("IAAT_FORCE_CSMEM") : -1;
+    bool tuned = false;
+    if (!kn.any() && !r.ptr_array && !std::getenv("IAAT_NO_TUNING")) {
+        const int elt = r.dtype == 0 ? 4 : 8;
+        const int64_t colsA = r.transA ? r.M : r.K, colsB = r.transB ? r.K : r.N;
+        const bool packed = r.batch <= 1 || (r.sA == r.lda * colsA && r.sB == r.ldb * colsB && r.sC == r.ldc * r.N);
+        auto al16 = [&](int64_t el) { return (el * elt) % 16 == 0; };
+        const bool vec = r.align % 16 == 0 && al16(r.lda) && al16(r.ldb) && al16(r.ldc) &&
+                         (r.batch <= 1 || (al16(r.sA) && al16(r.sB) && al16(r.sC)));
+        TunedKey k{{r.dtype, r.transA, r.transB, (int)r.M, (int)r.N, (int)r.K, (int)r.lda, (int)r.ldb, (int)r.ldc,
+                    packed ? 1 : 0, r.beta_zero, vec ? 1 : 0}};
+        const auto &t = tuning_table();
+        auto it = t.find(k);
+        if (it != t.end()) {
+            kn = it->second;
+            tuned = true;
+        }
+    }
+    Plan p = make_plan_knobs(r, kn);
+    if (p.status != 0 && kn.any()) p = make_plan_knobs(r, Knobs());
+    else p.tuned = tuned;
+    return p;
+}
+
+Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn)
 {
     Plan plan;
     const int elt = r.dtype == 0 ? 4 : 8;
@@ -307,17 +447,12 @@ Plan make_plan(const PlanRequest &r)
     const double hbm_per_problem = (double)(M * K + K * N + M * N * (r.beta_zero ? 1 : 2)) * elt;
     const int64_t sAb = r.sA * elt, sBb = r.sB * elt, sCb = r.sC * elt;
 
-    // Test/tuning knobs (never needed in production): force P, S, CTAs/SM,
-    // the first strip sizes or the family, e.g. IAAT_FORCE_P=4 IAAT_FORCE_TILE=8x8.
-    auto envi = [](const char *n) { const char *v = std::getenv(n); return v ? std::atoi(v) : 0; };
-    const int force_p = envi("IAAT_FORCE_P"), force_s = envi("IAAT_FORCE_S"), force_c = envi("IAAT_FORCE_CTAS");
-    int force_mr = 0, force_nr = 0;
-    if (const char *ft = std::getenv("IAAT_FORCE_TILE")) std::sscanf(ft, "%dx%d", &force_mr, &force_nr);
-    const int force_fam = std::getenv("IAAT_FORCE_FAMILY") ? envi("IAAT_FORCE_FAMILY") : -1;
-    const int force_order = std::getenv("IAAT_FORCE_ORDER") ? envi("IAAT_FORCE_ORDER") : -1;
+    const int force_s = kn.s, force_c = kn.ctas, force_mr = kn.mr, force_nr = kn.nr;
+    const int force_fam = kn.fam, force_order = kn.order;
 
     Candidate best;
     const int64_t pmax_batch = std::max<int64_t>(1, (r.batch + r.sm_count - 1) / r.sm_count);
+    const int force_p = kn.p > 0 ? (int)std::min<int64_t>(kn.p, pmax_batch) : 0;
 
     // Evaluate one (tiling, P, CTAs/SM) point.  `warp_instr`, `warp_wf`,
     // `single`: per-group totals of the compute warps (see ClassCost).
@@ -328,7 +463,7 @@ Plan make_plan(const PlanRequest &r)
         stage_layout(geo.spanB, sBb, P, r.ptr_array, c.modeB, c.slotB, c.capB);
         c.capC = 0;
         c.c_in_smem = 0;
-        if (!r.beta_zero) {  // C_in rides in the stage with A and B (read from smem in the epilogue)
+        if (!r.beta_zero && kn.csmem != 0) {  // C_in rides in the stage with A and B (read from smem)
             stage_layout(geo.spanC, sCb, P, r.ptr_array, c.modeC, c.slotC, c.capC);
             c.c_in_smem = 1;
         }
@@ -384,7 +519,13 @@ Plan make_plan(const PlanRequest &r)
             bool avail = true;
             int64_t memops = 2 * M * N;
             int area = 0;
-            struct C4 { int mr, nr, tiles, tm, tn, rb, cb, order; ClassCost cost; } cl[4];
+            // mapping options per class: linear row-/column-fastest, blocked bm x 32/bm
+            static const int kMaps[8] = {-2, -1, 1, 2, 4, 8, 16, 32};
+            struct C4 {
+                int mr, nr, tiles, tm, tn, rb, cb;
+                ClassCost cost[8];
+                bool ok[8];
+            } cl[4];
             int ncl = 0;
             int rb = 0;
             for (int a = 0; a < ms.n && avail; ++a) {
@@ -396,21 +537,29 @@ Plan make_plan(const PlanRequest &r)
                         break;
                     }
                     const int tm = ms.s[a].count, tn = ns.s[b].count;
-                    C4 q{mr, nr, tm * tn, tm, tn, rb, cb, 0, {}};
-                    // lane order: the cheaper of row-fastest / column-fastest
-                    double bestc = 1e300;
-                    for (int order = 0; order < 2; ++order) {
-                        if (force_order >= 0 && order != force_order) continue;
-                        ClassCost cc = fma_class_cost(r, vec, elt, mr, nr, tm * tn, tm, tn, rb, cb, order,
-                                                      pstrideA, pstrideB, pstrideC);
-                        const double key = std::max(cc.instr / kIssuePerClk, cc.wf);
-                        if (key < bestc * 0.999) {
-                            bestc = key;
-                            q.order = order;
-                            q.cost = cc;
+                    C4 &q = cl[ncl++];
+                    q.mr = mr;
+                    q.nr = nr;
+                    q.tiles = tm * tn;
+                    q.tm = tm;
+                    q.tn = tn;
+                    q.rb = rb;
+                    q.cb = cb;
+                    for (int m = 0; m < 8; ++m) {
+                        const int map = kMaps[m];
+                        q.ok[m] = true;
+                        if (force_order >= 0 && !((force_order == 0 && map == -2) || (force_order == 1 && map == -1) ||
+                                                  (force_order >= 2 && map == force_order - 1)))
+                            q.ok[m] = false;
+                        // a blocked warp must stay inside one problem and be mostly busy
+                        if (map > 0) {
+                            Lanes L = lane_map(map, q.tiles, tm, tn);
+                            if (L.active < 24 || q.tiles < 32) q.ok[m] = false;
                         }
+                        if (!q.ok[m]) continue;
+                        Lanes L = lane_map(map, q.tiles, tm, tn);
+                        q.cost[m] = fma_class_cost(r, vec, elt, mr, nr, L, rb, cb, pstrideA, pstrideB, pstrideC);
                     }
-                    cl[ncl++] = q;
                     memops += (int64_t)tm * tn * (mr + nr) * K;
                     area = std::max(area, mr * nr);
                     cb += ns.s[b].size * ns.s[b].count;
@@ -418,7 +567,7 @@ Plan make_plan(const PlanRequest &r)
                 rb += ms.s[a].size * ms.s[a].count;
             }
             if (!avail) continue;
-            for (int ctas = 1; ctas <= 2; ++ctas) {
+            for (int ctas = 1; ctas <= 4; ++ctas) {
                 if (force_c && ctas != force_c) continue;
                 const int wmax = IAAT_MAX_THREADS / 32 / ctas - 1;
                 for (int P = 1; P <= 1024; ++P) {
@@ -426,13 +575,33 @@ Plan make_plan(const PlanRequest &r)
                     if (force_p && P != force_p) continue;
                     int W = 0;
                     double instr = 0, wf = 0, single = 0;
+                    int pick[4];
+                    bool fits = true;
                     for (int q = 0; q < ncl; ++q) {
-                        const int w = (P * cl[q].tiles + 31) / 32;
+                        // cheapest mapping of this class at this P
+                        double bestk = 1e300;
+                        pick[q] = -1;
+                        for (int m = 0; m < 8; ++m) {
+                            if (!cl[q].ok[m]) continue;
+                            const int w = class_warps(kMaps[m], P, cl[q].tiles, cl[q].tm, cl[q].tn);
+                            const double k =
+                                w * std::max(cl[q].cost[m].instr / kIssuePerClk, cl[q].cost[m].wf / kSmemPerClk);
+                            if (k < bestk * 0.999) {
+                                bestk = k;
+                                pick[q] = m;
+                            }
+                        }
+                        if (pick[q] < 0) {
+                            fits = false;
+                            break;
+                        }
+                        const int w = class_warps(kMaps[pick[q]], P, cl[q].tiles, cl[q].tm, cl[q].tn);
                         W += w;
-                        instr += w * cl[q].cost.instr;
-                        wf += w * cl[q].cost.wf;
-                        single = std::max(single, cl[q].cost.single);
+                        instr += w * cl[q].cost[pick[q]].instr;
+                        wf += w * cl[q].cost[pick[q]].wf;
+                        single = std::max(single, cl[q].cost[pick[q]].single);
                     }
+                    if (!fits) continue;
                     if (W > wmax) break;
                     double pipe = 0;
                     if (r.dtype == 1) pipe = (double)P * M * N * K / kDfmaPerClk;
@@ -448,10 +617,11 @@ Plan make_plan(const PlanRequest &r)
                     int wb = 0;
                     c.ncls = ncl;
                     for (int q = 0; q < ncl; ++q) {
-                        const int w = (P * cl[q].tiles + 31) / 32;
+                        const int map = kMaps[pick[q]];
+                        const int w = class_warps(map, P, cl[q].tiles, cl[q].tm, cl[q].tn);
                         c.cls[q] = IaatClass{catalog_code(IAAT_FAM_FMA, cl[q].mr, cl[q].nr), wb, wb + w,
                                              cl[q].tiles, cl[q].tm, cl[q].rb, cl[q].mr, cl[q].cb, cl[q].nr,
-                                             cl[q].tn, cl[q].order};
+                                             cl[q].tn, map == -1 ? 1 : 0, map > 0 ? map : 0};
                         wb += w;
                     }
                     best = c;
@@ -474,7 +644,7 @@ Plan make_plan(const PlanRequest &r)
                 const double kst = (double)((K + 3) / 4);
                 const double instr_item = kst * (wm * wn + wm + wn + 2) + wm * wn * (r.beta_zero ? 6 : 10) + 30;
                 const double wf_item = kst * (wm + wn) * 4.0 + wm * wn * (r.beta_zero ? 0 : 2);
-                for (int ctas = 1; ctas <= 2; ++ctas) {
+                for (int ctas = 1; ctas <= 4; ++ctas) {
                     if (force_c && ctas != force_c) continue;
                     const int wmax = IAAT_MAX_THREADS / 32 / ctas - 1;
                     for (int P = 1; P <= 64; ++P) {
@@ -502,7 +672,7 @@ Plan make_plan(const PlanRequest &r)
                             if (!better(c, best)) continue;
                             c.ncls = 1;
                             c.cls[0] = IaatClass{catalog_code(IAAT_FAM_DMMA, 8 * wm, 8 * wn), 0, W, tiles, tm,
-                                                 0, 8 * wm, 0, 8 * wn, tn, 0};
+                                                 0, 8 * wm, 0, 8 * wn, tn, 0, 0};
                             best = c;
                         }
                     }
@@ -582,6 +752,7 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
         return s;
     }
     const IaatKParams &k = p.kp;
+    add("\"tuned\": %d, ", p.tuned);
     add("\"family\": \"%s\", \"vec\": %d, \"P\": %d, \"S\": %d, \"compute_warps\": %d, \"ctas_per_sm\": %d, "
         "\"grid\": %d, \"block\": %d, \"smem\": %d, \"ngroups\": %lld, ",
         p.family == IAAT_FAM_DMMA ? "dmma" : "fma", p.vec, k.P, k.S, k.n_compute_warps, p.ctas, p.grid, p.block,
@@ -599,9 +770,9 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
     for (int q = 0; q < k.nclasses; ++q) {
         const IaatClass &c = k.cls[q];
         add("%s{\"code\": %d, \"mr\": %d, \"nr\": %d, \"tiles\": %d, \"tm\": %d, \"row_base\": %d, "
-            "\"col_base\": %d, \"warp_begin\": %d, \"warp_end\": %d, \"colfast\": %d}",
+            "\"col_base\": %d, \"warp_begin\": %d, \"warp_end\": %d, \"colfast\": %d, \"bm\": %d}",
             q ? ", " : "", c.code, c.mr, c.nr, c.tiles, c.tm, c.row_base, c.col_base, c.warp_begin,
-            c.warp_end, c.colfast);
+            c.warp_end, c.colfast, c.bm);
     }
     s += "]}";
     return s;

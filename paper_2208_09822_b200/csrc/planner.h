@@ -35,6 +35,7 @@ struct Plan {
     int vec = 0;           // kernel variant: 16-byte vector paths enabled
     int family = 0;        // IAAT_FAM_FMA or IAAT_FAM_DMMA
     int ctas = 1;          // resident CTAs per SM the plan is sized for
+    int tuned = 0;         // 1: knobs came from the install-time tuning table
     Strip mstrip[2]{}, nstrip[2]{};
     int nm = 0, nn = 0;    // strips used per dimension
     int64_t memops = 0;    // paper cost: sum_i (m_i + n_i) K + 2 M N

@@ -1,0 +1,261 @@
+"""Install-time tuning on a B200 (run once per machine type, result committed).
+
+    python -m paper_2208_09822_b200.tune --config 2 [--config 3 ...] [--out .../tuning/b200.tsv]
+
+The paper's install-time stage "automatically tunes kernels based on
+features of the hardware" (Sec. I; Sec. III-A).
+Here the hardware-dependent choices are the run-time planner's knobs: the
+main micro-tile of the exact decomposition, problems per stage P, pipeline
+stages S, CTAs per SM and the lane -> tile mapping.  For each input of a
+workload this script times candidate plans through the public C ABI (forced
+with the IAAT_FORCE_* knobs the planner understands), keeps the fastest, and
+writes one line per input to tuning/b200.tsv, which libiaat.so reads at run
+time (key: dtype, transposition, M, N, K, ld's, packed strides, beta == 0,
+16-byte alignment).  Inputs not in the table fall back to the planner's cost
+model.  Tuning only changes speed: every candidate computes the same
+bitwise-identical result (one fixed-order FMA chain per element).
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+DEFAULT_OUT = os.path.join(PKG, "tuning", "b200.tsv")
+KNOBS = ("IAAT_FORCE_TILE", "IAAT_FORCE_P", "IAAT_FORCE_S", "IAAT_FORCE_CTAS", "IAAT_FORCE_ORDER",
+         "IAAT_FORCE_FAMILY", "IAAT_FORCE_CSMEM")
+S3 = [1, 3, 5, 7, 11, 13, 17, 23, 31, 37, 47, 53, 61, 67, 79]
+
+
+def config_shapes(cfg):
+    """(dtype, trans, M, N, K, batch, alpha, beta) of BASELINE.json's configs."""
+    out = []
+    if cfg == 1:
+        out.append(("f32", "NN", 16, 16, 16, 2000, 1.0, 0.0))
+    elif cfg == 2:
+        for n in range(4, 81, 4):
+            for tr in ("NN", "NT", "TT"):
+                out.append(("f32", tr, n, n, n, (256 << 20) // (12 * n * n), 1.5, 0.5))
+    elif cfg == 3:
+        triples = [(m, n, k) for m in S3 for n in S3 for k in S3 if m * n * k <= 512000]
+        rng = np.random.default_rng(2)
+        for i in rng.choice(len(triples), size=64, replace=False):
+            m, n, k = triples[i]
+            out.append(("f32", "NN", m, n, k, 100000, 1.0, 1.0))
+    elif cfg == 4:
+        for n in range(2, 33):
+            out.append(("f32", "TN", n, n, n, 500000, -1.0, 0.25))
+        out += [("f32", "TN", 32, 32, 2, 500000, -1.0, 0.25), ("f32", "TN", 2, 32, 32, 500000, -1.0, 0.25)]
+    elif cfg == 5:
+        for n in (8, 16, 32, 48, 64, 80):
+            for tr in ("NN", "NT"):
+                out.append(("f64", tr, n, n, n, 2_000_000, 1.0, 0.0))
+    return out
+
+
+def set_knobs(**kw):
+    for k in KNOBS:
+        os.environ.pop(k, None)
+    for k, v in kw.items():
+        if v is not None:
+            os.environ["IAAT_FORCE_" + k.upper()] = str(v)
+
+
+class Bench:
+    """One input of the workload, with NSETS independent operand sets used
+    round-robin so that consecutive timed calls never find the previous
+    call's operands in L2 (each set is >= 2x the 126 MB L2 or the full
+    workload batch, whichever is smaller)."""
+    NSETS = 3
+
+    def __init__(self, dtype, tr, M, N, K, batch, alpha, beta, max_bytes=3 << 30):
+        import torch
+        import datagen
+        self.torch = torch
+        self.dt = 0 if dtype == "f32" else 1
+        elt = 4 if dtype == "f32" else 8
+        self.tr, self.M, self.N, self.K, self.alpha, self.beta = tr, M, N, K, alpha, beta
+        ra, ca = (M, K) if tr[0] == "N" else (K, M)
+        rb, cb = (K, N) if tr[1] == "N" else (N, K)
+        per = (ra * ca + rb * cb + M * N) * elt
+        self.batch = int(min(batch, max(1, max_bytes // per)))
+        self.ra, self.ca, self.rb, self.cb = ra, ca, rb, cb
+        tdt = torch.float32 if elt == 4 else torch.float64
+        nsets = self.NSETS if self.batch * per < (1 << 30) else 1
+        self.sets = []
+        for i in range(nsets):
+            A = torch.empty(self.batch * ra * ca, dtype=tdt, device="cuda")
+            B = torch.empty(self.batch * rb * cb, dtype=tdt, device="cuda")
+            C = torch.empty(self.batch * M * N, dtype=tdt, device="cuda")
+            datagen.fill_device(A, 9 + i, 0, ra, ca, ra, ra * ca, self.batch)
+            datagen.fill_device(B, 9 + i, 1, rb, cb, rb, rb * cb, self.batch)
+            datagen.fill_device(C, 9 + i, 2, M, N, M, M * N, self.batch)
+            self.sets.append((A, B, C))
+        self.turn = 0
+
+    def plan(self):
+        from paper_2208_09822_b200 import iaat
+        return iaat.iaat_plan_describe(self.dt, self.tr[0], self.tr[1], self.M, self.N, self.K, self.ra,
+                                       self.ra * self.ca, self.rb, self.rb * self.cb, self.M, self.M * self.N,
+                                       self.batch, self.beta == 0)
+
+    def call(self):
+        from paper_2208_09822_b200 import iaat
+        A, B, C = self.sets[self.turn % len(self.sets)]
+        self.turn += 1
+        st = iaat.iaat_gemm_strided_batched(self.dt, self.tr[0], self.tr[1], self.M, self.N, self.K, self.alpha,
+                                            A.data_ptr(), self.ra, self.ra * self.ca, B.data_ptr(),
+                                            self.rb, self.rb * self.cb, self.beta, C.data_ptr(), self.M,
+                                            self.M * self.N, self.batch,
+                                            self.torch.cuda.current_stream().cuda_stream)
+        if st != 0:
+            raise RuntimeError("status %d" % st)
+
+    def time_us(self, reps=6, warm=3):
+        torch = self.torch
+        for _ in range(warm):
+            self.call()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            self.call()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / reps
+
+    def free(self):
+        del self.sets
+        self.torch.cuda.empty_cache()
+
+
+def key_line(dt, tr, M, N, K, beta0, vec=1):
+    ra = M if tr[0] == "N" else K
+    rb = K if tr[1] == "N" else N
+    return "%d %d %d %d %d %d %d %d %d %d %d %d" % (dt, tr[0] == "T", tr[1] == "T", M, N, K, ra, rb, M, 1,
+                                                     int(beta0), vec)
+
+
+def tile_options(M, N):
+    ms = sorted({x for x in (1, 2, 3, 4, 5, 6, 7, 8) if x <= M and (x in (2, 4, 8) or x == M or M < 8)})
+    ns = sorted({x for x in (1, 2, 3, 4, 5, 6, 7, 8) if x <= N and (x in (2, 4, 8) or x == N or N < 8)})
+    return [(a, b) for a in ms for b in ns]
+
+
+def tune_shape(sh, log):
+    dtype, tr, M, N, K, batch, alpha, beta = sh
+    elt = 4 if dtype == "f32" else 8
+    b = Bench(*sh)
+    results = []  # (us, knobs dict)
+
+    def trial(**kw):
+        set_knobs(**kw)
+        try:
+            p = b.plan()
+            if p["status"] != 0:
+                return None
+            us = b.time_us()
+        except Exception:
+            return None
+        finally:
+            set_knobs()
+        results.append((us, kw, p))
+        return us
+
+    auto = trial()
+    per = (M * K + K * N + (0 if beta == 0 else M * N)) * elt
+    Ps = sorted({max(1, int(kb * 1024) // per) for kb in (12, 24, 40, 64, 96)})
+    for (mr, nr) in tile_options(M, N):
+        for P in Ps:
+            trial(tile="%dx%d" % (mr, nr), p=P)
+    if dtype == "f64" and M % 8 == 0 and N % 8 == 0:
+        for (wm, wn) in ((1, 1), (1, 2), (2, 1), (2, 2)):
+            for P in Ps:
+                trial(tile="%dx%d" % (8 * wm, 8 * wn), p=P, family=1)
+    if beta != 0:  # C_in from global (L2-prefetched) instead of staged: frees smem
+        per_ab = (M * K + K * N) * elt
+        for (mr, nr) in tile_options(M, N):
+            for P in sorted({max(1, int(kb * 1024) // per_ab) for kb in (24, 48, 96)}):
+                trial(tile="%dx%d" % (mr, nr), p=P, csmem=0)
+    results.sort(key=lambda x: x[0])
+    top = results[:4]
+    for us, kw, p in top:
+        for order in (0, 1, 3, 5, 9, 17):
+            for ctas in (1, 2, 3, 4):
+                for s in (0, 2, 3):
+                    kk = dict(kw)
+                    kk.update(order=order, ctas=ctas)
+                    if s:
+                        kk["s"] = s
+                    trial(**kk)
+    results.sort(key=lambda x: x[0])
+    best_us, best_kw, best_p = results[0]
+    b.free()
+    if auto is not None and auto <= best_us * 1.01:
+        best_kw, best_us = {}, auto
+    byts = (M * K + K * N + M * N * (1 if beta == 0 else 2)) * elt * b.batch
+    log("%s %s %dx%dx%d batch=%d auto=%.1fus best=%.1fus (%.0f GB/s, %.0f GFLOP/s) knobs=%s" % (
+        dtype, tr, M, N, K, b.batch, auto or -1, best_us, byts / best_us / 1e3,
+        2.0 * M * N * K * b.batch / best_us / 1e3, best_kw))
+    return best_kw, best_p
+
+
+def knobs_to_line(kw, p):
+    """Knobs of the winning plan as the planner's table fields."""
+    mr, nr = (int(x) for x in kw["tile"].split("x")) if "tile" in kw else (0, 0)
+    return "%d %d %d %d %d %d %d %d" % (mr, nr, kw.get("p", 0), kw.get("s", 0), kw.get("ctas", 0),
+                                        kw.get("order", -1), kw.get("family", -1), kw.get("csmem", -1))
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, action="append", default=[])
+    ap.add_argument("--out", default=DEFAULT_OUT)
+    ap.add_argument("--log", default=None)
+    ap.add_argument("--min-n", type=int, default=0, help="only inputs with max(M,N,K) >= this")
+    ap.add_argument("--max-n", type=int, default=1 << 30)
+    a = ap.parse_args(argv)
+    sys.path.insert(0, ROOT)
+    os.environ["IAAT_NO_TUNING"] = "1"  # tune against the cost model, not an older table
+    existing = {}
+    if os.path.exists(a.out):
+        for ln in open(a.out):
+            if ln.startswith("#") or ":" not in ln:
+                continue
+            k, v = ln.split(":", 1)
+            existing[k.strip()] = v.strip()
+    logf = open(a.log, "a") if a.log else None
+
+    def log(s):
+        print(s, flush=True)
+        if logf:
+            logf.write(s + "\n")
+            logf.flush()
+
+    t0 = time.time()
+    for cfg in a.config or [2]:
+        for sh in config_shapes(cfg):
+            if not a.min_n <= max(sh[2:5]) <= a.max_n:
+                continue
+            kw, p = tune_shape(sh, log)
+            dtype, tr, M, N, K, batch, alpha, beta = sh
+            key = key_line(0 if dtype == "f32" else 1, tr, M, N, K, beta == 0)
+            if kw:
+                existing[key] = knobs_to_line(kw, p)
+            else:
+                existing.pop(key, None)
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    with open(a.out, "w") as f:
+        f.write("# install-time tuning table for libiaat.so on B200 (written by paper_2208_09822_b200/tune.py)\n")
+        f.write("# dtype tA tB M N K lda ldb ldc packed beta0 vec : mr nr P S ctas order family csmem\n")
+        for k in sorted(existing):
+            f.write("%s : %s\n" % (k, existing[k]))
+    log("tuned %d entries in %.0fs -> %s" % (len(existing), time.time() - t0, a.out))
+
+
+if __name__ == "__main__":
+    main()

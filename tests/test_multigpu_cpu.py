@@ -1,0 +1,94 @@
+"""Multi-GPU path on CPU: world-size-2 gloo processes shard a batch by
+contiguous ranges (paper_2208_09822_b200.dist), each computes its shard with
+the CPU oracle standing in for its GPU, and the gathered result must equal the
+unsharded computation bitwise; the bench's max-over-ranks timing reduction is
+exercised over the same process group.  No collective touches the data path
+in the product -- the all_gather here is only the test's check."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2208_09822_b200.dist import aggregate_gflops, shard_range, weak_range
+
+
+def test_shard_range_partitions():
+    for total in (0, 1, 7, 2_000_000, 12345):
+        for world in (1, 2, 3, 4, 8):
+            cuts = [shard_range(total, r, world) for r in range(world)]
+            assert cuts[0][0] == 0 and cuts[-1][1] == total
+            for (a, b), (c, d) in zip(cuts[:-1], cuts[1:]):
+                assert b == c and a <= b
+            sizes = [b - a for a, b in cuts]
+            assert max(sizes) - min(sizes) <= 1
+    assert weak_range(100, 3) == (300, 400)
+    assert aggregate_gflops([2e9, 2e9], [1.0, 2.0]) == 2.0
+    with pytest.raises(ValueError):
+        shard_range(10, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import datagen
+    import oracle
+    M, N, K, total = 7, 5, 9, 101
+    lo, hi = shard_range(total, rank, world)
+    ids = np.arange(lo, hi)
+    A = datagen.fill_host(3, 0, np.float32, M, K, M, M * K, ids)
+    B = datagen.fill_host(3, 1, np.float32, K, N, K, K * N, ids)
+    C = datagen.fill_host(3, 2, np.float32, M, N, M, M * N, ids)
+    ref, _, _ = oracle.ref_gemm("N", "N", M, N, K, 1.5, A, M, M * K, B, K, K * N, 0.5, C, M, M * N, len(ids),
+                                nthreads=1)
+    # pad to equal length for all_gather
+    maxn = max(shard_range(total, r, world)[1] - shard_range(total, r, world)[0] for r in range(world))
+    buf = torch.full((maxn, N, M), float("nan"), dtype=torch.float64)
+    buf[:len(ids)] = torch.from_numpy(ref)
+    gathered = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(gathered, buf)
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)  # bench.py's max-over-ranks time
+    if rank == 0:
+        parts = []
+        for r in range(world):
+            a, b = shard_range(total, r, world)
+            parts.append(gathered[r][:b - a].numpy())
+        out.put((np.concatenate(parts), float(t.item())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_shards_match_unsharded():
+    import datagen
+    import oracle
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    sharded, tmax = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    M, N, K, total = 7, 5, 9, 101
+    ids = np.arange(total)
+    A = datagen.fill_host(3, 0, np.float32, M, K, M, M * K, ids)
+    B = datagen.fill_host(3, 1, np.float32, K, N, K, K * N, ids)
+    C = datagen.fill_host(3, 2, np.float32, M, N, M, M * N, ids)
+    ref, _, _ = oracle.ref_gemm("N", "N", M, N, K, 1.5, A, M, M * K, B, K, K * N, 0.5, C, M, M * N, total)
+    assert np.array_equal(sharded, ref)
+    assert tmax == 2.0
