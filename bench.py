@@ -190,7 +190,7 @@ def run_ours(args, rank, world, local_rank):
         ra, ca, rb, cb = s.stored()
         per = (ra * ca + rb * cb + s.M * s.N) * s.elt
         cap = int(0.80 * hbm_cap) // (per * 2 if s.dtype == "f64" else per * 3)  # keep room for others
-        cnt = s.batch if args.config != 5 else min(s.batch, max(1, int(0.70 * hbm_cap) // per))
+        cnt = s.batch if args.config != 5 else min(s.batch, max(1, int(0.60 * hbm_cap) // per))
         for lo in range(0, s.batch, cnt):
             chunks.append((s, lo, min(cnt, s.batch - lo)))
         _ = cap
@@ -212,6 +212,7 @@ def run_ours(args, rank, world, local_rank):
         bufs[key] = (A, B, C)
         if args.config == 5:
             break  # config 5 re-fills per chunk inside the step loop (generation untimed, see below)
+    A = B = C = None  # only bufs holds the operand sets (config 5 frees them chunk by chunk)
     torch.cuda.synchronize()
 
     def call(s, lo, cnt):
@@ -332,9 +333,11 @@ def run_chunked_config5(args, rank, world, local_rank, shapes, desc, chunks, buf
     n_launch = 0
     clocks = ClockSampler(local_rank)
     clocks.start()
+    A = B = C = None
     for s, lo, cnt in chunks:
         key = (s.dtype, s.M, s.N, s.K, s.tr, cnt)
         if key not in bufs:
+            A = B = C = None  # drop every reference before freeing
             bufs.clear()
             torch.cuda.empty_cache()
             ra, ca, rb, cb = s.stored()

@@ -15,7 +15,7 @@
 //        A'(g, t) = op(B)(k0+t, col0+g)
 //   B' fragment (4x8, col): lane holds B'(t, g) = op(A)(row0+g, k0+t)
 //   D' (8x8): lane holds D'(g, 2t+h) = C(row0 + 2t + h, col0 + g), h = 0, 1
-// K % 4 tail: the missing k of the last step are zero in BOTH fragments
+// K % 8 tail: the missing k of the last steps are zero in BOTH fragments
 // (0*0 adds nothing); no MMA is predicated.
 #pragma once
 #include "iaat_device.cuh"
@@ -29,54 +29,77 @@ __device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, dou
                  : "d"(a), "d"(b));
 }
 
-template <bool TA, bool TB, int WM, int WN>
+// K is consumed 8 at a time as two DMMA k-steps.  The MMA sums its 4
+// k-positions in any order, so position t of step h is given the actual k
+// k0 + 2t + h (the same for every row/column -- consistent between the two
+// fragments): a lane's two k-values are ADJACENT, and for an operand that is
+// contiguous along k one 16-byte load (LDS.128) feeds both steps.
+template <bool KCONTIG, bool VEC>
+__device__ __forceinline__ void dmma_pair(const double *__restrict__ X, int off, int ld, int k0, int t, int K,
+                                          bool full, double &v0, double &v1)
+{
+    const int k = k0 + 2 * t;
+    if (KCONTIG) {
+        const double *p = X + off + k;  // element (k, r) at X[k + r*ld], off = r*ld
+        if (full) {
+            if (VEC) {
+                double2 d = *reinterpret_cast<const double2 *>(p);
+                v0 = d.x;
+                v1 = d.y;
+            } else {
+                v0 = p[0];
+                v1 = p[1];
+            }
+        } else {
+            v0 = k < K ? p[0] : 0.0;
+            v1 = k + 1 < K ? p[1] : 0.0;
+        }
+    } else {
+        const double *p = X + off + (int64_t)k * ld;  // element (r, k) at X[r + k*ld], off = r
+        if (full) {
+            v0 = p[0];
+            v1 = p[ld];
+        } else {
+            v0 = k < K ? p[0] : 0.0;
+            v1 = k + 1 < K ? p[ld] : 0.0;
+        }
+    }
+}
+
+template <bool TA, bool TB, int WM, int WN, bool VEC>
 __device__ __forceinline__ void dmma_tile(double (&acc)[WM][WN][2], const double *__restrict__ sA,
                                           const double *__restrict__ sB, int lda, int ldb, int K,
                                           int row0, int col0, int g, int t)
 {
-    // element addresses relative to k = 0
+    // op(A)(i,k): TA ? A[k + i*lda] (k-contiguous) : A[i + k*lda]
+    // op(B)(k,j): TB ? B[j + k*ldb] : B[k + j*ldb] (k-contiguous)
     int aoff[WM], boff[WN];
 #pragma unroll
     for (int mi = 0; mi < WM; ++mi) {
         const int r = row0 + 8 * mi + g;
-        aoff[mi] = TA ? (t + r * lda) : (r + t * lda);
+        aoff[mi] = TA ? r * lda : r;
     }
 #pragma unroll
     for (int nj = 0; nj < WN; ++nj) {
         const int cidx = col0 + 8 * nj + g;
-        boff[nj] = TB ? (cidx + t * ldb) : (t + cidx * ldb);
+        boff[nj] = TB ? cidx : cidx * ldb;
     }
-    const int astep = TA ? 4 : 4 * lda;  // address step per k-step of 4
-    const int bstep = TB ? 4 * ldb : 4;
-    const int kfull = K & ~3;
-    int k0 = 0;
-#pragma unroll 2
-    for (; k0 < kfull; k0 += 4) {
-        double af[WM], bf[WN];
+    const int kfull = K & ~7;
+#pragma unroll 1
+    for (int k0 = 0; k0 < K; k0 += 8) {
+        const bool full = k0 < kfull;
+        double af[WM][2], bf[WN][2];
 #pragma unroll
-        for (int mi = 0; mi < WM; ++mi) af[mi] = sA[aoff[mi]];
+        for (int mi = 0; mi < WM; ++mi) dmma_pair<TA, VEC>(sA, aoff[mi], lda, k0, t, K, full, af[mi][0], af[mi][1]);
 #pragma unroll
-        for (int nj = 0; nj < WN; ++nj) bf[nj] = sB[boff[nj]];
+        for (int nj = 0; nj < WN; ++nj) dmma_pair<!TB, VEC>(sB, boff[nj], ldb, k0, t, K, full, bf[nj][0], bf[nj][1]);
 #pragma unroll
-        for (int mi = 0; mi < WM; ++mi) aoff[mi] += astep;
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int nj = 0; nj < WN; ++nj) boff[nj] += bstep;
+            for (int mi = 0; mi < WM; ++mi)
 #pragma unroll
-        for (int mi = 0; mi < WM; ++mi)
-#pragma unroll
-            for (int nj = 0; nj < WN; ++nj) dmma_8x8x4(acc[mi][nj][0], acc[mi][nj][1], bf[nj], af[mi]);
-    }
-    if (k0 < K) {  // K % 4 tail: zero-fill the k >= K lanes of both fragments
-        const bool valid = k0 + t < K;
-        double af[WM], bf[WN];
-#pragma unroll
-        for (int mi = 0; mi < WM; ++mi) af[mi] = valid ? sA[aoff[mi]] : 0.0;
-#pragma unroll
-        for (int nj = 0; nj < WN; ++nj) bf[nj] = valid ? sB[boff[nj]] : 0.0;
-#pragma unroll
-        for (int mi = 0; mi < WM; ++mi)
-#pragma unroll
-            for (int nj = 0; nj < WN; ++nj) dmma_8x8x4(acc[mi][nj][0], acc[mi][nj][1], bf[nj], af[mi]);
+                for (int nj = 0; nj < WN; ++nj)
+                    dmma_8x8x4(acc[mi][nj][0], acc[mi][nj][1], bf[nj][h], af[mi][h]);
     }
 }
 
@@ -117,7 +140,7 @@ __device__ __forceinline__ void dmma_class_loop(const IaatKParams &p, const Iaat
             for (int mi = 0; mi < WM; ++mi)
 #pragma unroll
                 for (int nj = 0; nj < WN; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
-            dmma_tile<TA, TB, WM, WN>(acc, sA, sB, p.lda, p.ldb, p.K, row0, col0, g, t);
+            dmma_tile<TA, TB, WM, WN, VEC>(acc, sA, sB, p.lda, p.ldb, p.K, row0, col0, g, t);
             const char *c_first = prob_ptr(p.C, cptrs(p), scb, b0);
             const char *c_prob = prob_ptr(p.C, cptrs(p), scb, b0 + pl);
             double *C = const_cast<double *>(reinterpret_cast<const double *>(c_prob));

@@ -632,8 +632,8 @@ Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn)
 
     // ------------------------------------------------------------ DMMA family (fp64)
     if (r.dtype == 1 && M % 8 == 0 && N % 8 == 0 && !(force_fam >= 0 && force_fam != IAAT_FAM_DMMA)) {
-        for (int wm = 1; wm <= 2; ++wm)
-            for (int wn = 1; wn <= 2; ++wn) {
+        for (int wm = 1; wm <= 4; wm *= 2)
+            for (int wn = 1; wn <= 4; wn *= 2) {
                 if ((M / 8) % wm || (N / 8) % wn) continue;
                 if (force_mr && (8 * wm != force_mr || 8 * wn != force_nr)) continue;
                 if (!catalog_has(1, tidx, IAAT_FAM_DMMA, 8 * wm, 8 * wn)) continue;
@@ -641,9 +641,13 @@ Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn)
                 const int tiles = tm * tn;
                 const int64_t memops = (int64_t)tiles * (8 * wm + 8 * wn) * K + 2 * M * N;
                 // per item (one warp tile over K): DMMAs + fragment loads + epilogue
-                const double kst = (double)((K + 3) / 4);
-                const double instr_item = kst * (wm * wn + wm + wn + 2) + wm * wn * (r.beta_zero ? 6 : 10) + 30;
-                const double wf_item = kst * (wm + wn) * 4.0 + wm * wn * (r.beta_zero ? 0 : 2);
+                // per 8 k: 2 WM WN DMMAs, one LDS.128 per k-contiguous fragment
+                // (two LDS.64 otherwise), ~6 wavefronts per fragment pair
+                const double kst = (double)((K + 7) / 8);
+                const double nla = r.transA ? 1.0 : 2.0, nlb = r.transB ? 2.0 : 1.0;
+                const double instr_item =
+                    kst * (2 * wm * wn + wm * nla + wn * nlb + 4) + wm * wn * (r.beta_zero ? 6 : 10) + 30;
+                const double wf_item = kst * (wm + wn) * 6.0 + wm * wn * (r.beta_zero ? 0 : 2);
                 for (int ctas = 1; ctas <= 4; ++ctas) {
                     if (force_c && ctas != force_c) continue;
                     const int wmax = IAAT_MAX_THREADS / 32 / ctas - 1;
@@ -665,7 +669,7 @@ Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn)
                             c.memops = memops;
                             c.area = 64 * wm * wn;
                             c.W = W;
-                            const double single = per_warp * (instr_item + kst * 20.0) + 400.0;
+                            const double single = per_warp * (instr_item + kst * 40.0) + 400.0;
                             if (!evaluate(c, P, ctas, per_warp * W * instr_item, per_warp * W * wf_item, single,
                                           pipe))
                                 continue;

@@ -34,7 +34,13 @@ TRANS = ["NN", "NT", "TN", "TT"]
 MAX_MR = 8
 MAX_NR = 8
 # fp64 DMMA warp tiles: (wm, wn) DMMA.8x8x4 blocks per warp
-DMMA_TILES = [(1, 1), (1, 2), (2, 1), (2, 2)]
+DMMA_TILES = [(1, 1), (1, 2), (2, 1), (2, 2), (2, 4), (4, 2), (4, 4)]
+
+
+def dmma_tiles(tr):
+    """DMMA warp tiles (wm x wn blocks of 8x8) for a transposition; 4x4 would
+    spill in TN (both fragments loaded as 16-byte pairs plus 64 accumulators)."""
+    return [t for t in DMMA_TILES if not (tr == "TN" and t == (4, 4))]
 
 
 def fma_code(mr, nr):
@@ -42,7 +48,7 @@ def fma_code(mr, nr):
 
 
 def dmma_code(wm, wn):
-    return 100 + (wm - 1) * 2 + (wn - 1)
+    return 100 + 10 * wm + wn
 
 
 KU = {"f32": 4, "f64": 2}  # k-steps per unrolled block = one 16 B vector (csrc/iaat_device.cuh)
@@ -90,8 +96,8 @@ def catalog():
                 ents.append({"family": "fma", "dtype": dt, "trans": tr, "mr": mr, "nr": nr,
                              "code": fma_code(mr, nr)})
         if dt == "f64":
-            for wm, wn in DMMA_TILES:
-                for tr in TRANS:
+            for tr in TRANS:
+                for wm, wn in dmma_tiles(tr):
                     ents.append({"family": "dmma", "dtype": dt, "trans": tr, "mr": 8 * wm,
                                  "nr": 8 * wn, "code": dmma_code(wm, wn)})
     return ents
@@ -112,7 +118,7 @@ def gen_kernel_file(dt, tr, vec):
         cases.append("        case %d: fma_class_loop<%s, %s, %s, %d, %d, %s, %d>(p, c, smem, full, empty, warp, lane); break;"
                      % (fma_code(mr, nr), T, ta, tb, mr, nr, v, fma_unroll(dt, tr, mr, nr)))
     if dt == "f64":
-        for wm, wn in DMMA_TILES:
+        for wm, wn in dmma_tiles(tr):
             cases.append("        case %d: dmma_class_loop<%s, %s, %d, %d, %s>(p, c, smem, full, empty, warp, lane); break;"
                          % (dmma_code(wm, wn), ta, tb, wm, wn, v))
     inc = '#include "../iaat_device.cuh"\n'
@@ -180,7 +186,7 @@ def gen_catalog_inc(ents):
     lines = ["// GENERATED by gen/generate.py -- the install-time kernel catalog.",
              "#define IAAT_FMA_MAX_MR %d" % MAX_MR, "#define IAAT_FMA_MAX_NR %d" % MAX_NR,
              "#define IAAT_FMA_CODE(mr, nr) (((mr) - 1) * IAAT_FMA_MAX_NR + ((nr) - 1))",
-             "#define IAAT_DMMA_CODE(wm, wn) (100 + ((wm) - 1) * 2 + ((wn) - 1))",
+             "#define IAAT_DMMA_CODE(wm, wn) (100 + 10 * (wm) + (wn))",
              "struct IaatCatalogEntry { int family; int dtype; int trans; int mr; int nr; int code; };",
              "static const IaatCatalogEntry kCatalog[] = {"]
     for e in ents:
