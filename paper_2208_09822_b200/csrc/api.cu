@@ -4,6 +4,7 @@
 // single launch of the call's kernel executing plan on the caller's stream
 // (row a6).  There is no CPU fallback anywhere: a call
 // either enqueues sm_100a kernels or returns an error status.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -17,6 +18,7 @@
 
 #include "../../include/iaat.h"
 #include "iaat_device.cuh"
+#include "iaat_ks.cuh"
 #include "planner.h"
 
 #include "gen/kernel_table.inc"
@@ -165,6 +167,40 @@ double scalar(iaat_dtype_t dt, const void *p)
 
 bool elem_aligned(const void *p, int elt) { return (reinterpret_cast<uintptr_t>(p) % elt) == 0; }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time dependency on libcuda).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn()
+{
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// 3-D tile-mode tensor map of one operand (K-streamed family): dims
+// {stored rows, stored cols, batch}, the plan's box, zero fill out of bounds.
+bool encode_tmap(CUtensorMap &m, const TmaGeo &g, const void *base, int elt)
+{
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(&m, elt == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                    const_cast<void *>(base), g.dim, g.stride, g.box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    g.swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // alpha == 0 or K == 0 path: C = beta * C (or zeros).  A/B never read.
 iaat_status_t launch_scale(iaat_dtype_t dt, char *C, void *const *Carr, int64_t sC, int64_t M, int64_t N,
                            int64_t ldc, int64_t batch, double beta, cudaStream_t s, int sm_count)
@@ -242,6 +278,24 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
     const Plan &plan = cached_plan(r);
     if (plan.status != 0) return (iaat_status_t)plan.status;
 
+    if (plan.ks) {
+        IaatKsParams kp = plan.ksp;
+        kp.C = static_cast<char *>(C);
+        kp.alpha = a;
+        kp.beta = b;
+        alignas(64) CUtensorMap tmA, tmB;
+        if (!encode_tmap(tmA, plan.tmA, A, elt) || !encode_tmap(tmB, plan.tmB, B, elt)) {
+            g_last_cuda_error = (int)cudaErrorInvalidValue;
+            return IAAT_ERROR_CUDA;
+        }
+        cudaError_t e = kLaunchKs[r.dtype][ta * 2 + tb](tmA, tmB, kp, plan.grid, plan.block, plan.smem, s);
+        if (e != cudaSuccess) {
+            g_last_cuda_error = (int)e;
+            return IAAT_ERROR_CUDA;
+        }
+        g_launches.fetch_add(1);
+        return IAAT_SUCCESS;
+    }
     IaatKParams kp = plan.kp;
     kp.A = static_cast<const char *>(A);
     kp.B = static_cast<const char *>(B);

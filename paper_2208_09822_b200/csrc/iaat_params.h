@@ -21,8 +21,10 @@ enum IaatStage : int {
 
 // Micro-tile families of the install-time catalog.
 enum IaatFamily : int {
-    IAAT_FAM_FMA = 0,   // per-thread mr x nr FFMA/DFMA register tile
-    IAAT_FAM_DMMA = 1,  // per-warp (8*wm) x (8*wn) DMMA.8x8x4 tile (fp64 only)
+    IAAT_FAM_FMA = 0,     // per-thread mr x nr FFMA/DFMA register tile (slab staging)
+    IAAT_FAM_DMMA = 1,    // per-warp (8*wm) x (8*wn) DMMA.8x8x4 tile (fp64 only, slab staging)
+    IAAT_FAM_KS_FMA = 2,  // FMA tiles, K-streamed TMA staging (iaat_ks.cuh)
+    IAAT_FAM_KS_DMMA = 3, // DMMA warp tiles, K-streamed TMA staging (fp64 only)
 };
 
 // One tile class: all tiles of one exact size (mr x nr) inside one row strip
@@ -69,6 +71,33 @@ struct IaatKParams {
     int beta_zero;            // 1: C is write-only
     int c_in_smem;            // 1: C_in staged with A/B (beta != 0); 0 and beta != 0: read from global
     int prefetch_c;           // 1: producer prefetches the C span into L2 (when C_in is read from global)
+    int nclasses;
+    IaatClass cls[IAAT_MAX_CLASSES];
+};
+
+// ---------------------------------------------------------------- K-streamed family
+// Kernel executing plan of the "ks" kernels (iaat_ks.cuh): units of P
+// consecutive problems, streamed in K-chunks of kc elements through an
+// S-stage ring of TMA boxes.  The two CUtensorMaps travel as separate
+// __grid_constant__ kernel parameters.
+#define IAAT_KS_MAX_STAGES 12
+#define IAAT_KS_BAR_BYTES 256   // mbarriers; the stage ring starts at the next 1024 B boundary
+
+struct IaatKsParams {
+    char *C;
+    int64_t sC;          // C stride (elements)
+    int64_t batch;
+    int64_t nunits;      // ceil(batch / P)
+    double alpha, beta;
+    int M, N, K, ldc;
+    int P, S, kc, nchunks;
+    int n_compute_warps;
+    int a_pitch, b_pitch;  // MN-major operands: smem row pitch (elements) = TMA box inner dim
+    int a_bytes, b_bytes;  // smem bytes of one stage's A / B region (multiples of 1024)
+    int a_tx, b_tx;        // bytes one TMA box of A / B delivers (the full box)
+    int stage_bytes;       // a_bytes + b_bytes
+    int beta_zero;
+    int c_vec;             // 16-byte C accesses legal (C base, ldc, stride aligned)
     int nclasses;
     IaatClass cls[IAAT_MAX_CLASSES];
 };

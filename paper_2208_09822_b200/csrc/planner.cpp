@@ -421,8 +421,16 @@ Plan make_plan(const PlanRequest &r)
     return p;
 }
 
+bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out);
+
 Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn)
 {
+    if (kn.fam == IAAT_FAM_KS_FMA) {
+        Plan ksplan;
+        if (plan_ks(r, kn, ksplan)) return ksplan;
+        ksplan.status = 5;
+        return ksplan;
+    }
     Plan plan;
     const int elt = r.dtype == 0 ? 4 : 8;
     const int vw = 16 / elt;
@@ -740,6 +748,292 @@ Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn)
     return plan;
 }
 
+// ---------------------------------------------------------------- K-streamed family (iaat_ks.cuh)
+// Applicability: strided API; every base, ld and problem stride 16 B aligned
+// (TMA global-address rules); problems do not overlap; M, N <= 256 (box
+// extents).  Units of P problems stream through an S-stage ring of K-chunks
+// (kc = 128 B / elt); the same exact strip decomposition as the FMA family
+// gives the tile classes.
+namespace {
+
+struct KsCand {
+    bool ok = false;
+    double total = 1e300, unit = 0;
+    int P = 0, S = 0, W = 0, ctas = 1, a_bytes = 0, b_bytes = 0, a_pitch = 0, b_pitch = 0;
+    DimSplit ms, ns;
+    IaatClass cls[IAAT_MAX_CLASSES];
+    int ncls = 0;
+    int64_t memops = 0;
+};
+
+// smem wavefronts + instructions of one k-block (KU k-steps) of one warp of
+// a KS FMA class under lane mapping `map` (see lane_map).
+void ks_class_cost(const PlanRequest &r, int elt, int mr, int nr, const Lanes &L, int rb, int cb, int tm, int tn,
+                   int a_pitch, int b_pitch, int kc, double &instr, double &wf)
+{
+    const int VW = 16 / elt, KU = VW;
+    const bool AK = r.transA == 1, BK = r.transB == 0;
+    int64_t ad[32];
+    instr = (double)KU * mr * nr + 4;
+    wf = 0;
+    auto operand = [&](bool kmaj, int R, bool is_a) {
+        const int D = is_a ? (int)r.M : (int)r.N;
+        const int pitch = is_a ? a_pitch : b_pitch;
+        const int t_n = is_a ? tm : tn;
+        const int base = is_a ? rb : cb;
+        if (kmaj) {
+            for (int i = 0; i < R; ++i) {
+                for (int l = 0; l < 32; ++l) {
+                    const int t = is_a ? L.ti[l] : L.tj[l];
+                    const int64_t rab = (int64_t)L.pl[l] * D + base + t + t_n * i;
+                    ad[l] = rab * 128 + (((rab & 7)) << 4);
+                }
+                wf += wavefronts(ad, 16, 32);
+                instr += 2;  // LDS + XOR
+            }
+        } else {
+            const bool v = R % VW == 0;
+            for (int kk = 0; kk < KU; ++kk)
+                for (int q = 0; q < (v ? R / VW : R); ++q) {
+                    for (int l = 0; l < 32; ++l) {
+                        const int t = is_a ? L.ti[l] : L.tj[l];
+                        ad[l] = ((int64_t)L.pl[l] * kc * pitch + (int64_t)kk * pitch + base + t * R +
+                                 (v ? q * VW : q)) * elt;
+                    }
+                    wf += wavefronts(ad, v ? 16 : elt, 32);
+                    instr += 1;
+                }
+            instr += KU;  // row address adds
+        }
+    };
+    operand(AK, mr, true);
+    operand(BK, nr, false);
+}
+
+}  // namespace
+
+bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
+{
+    if (r.ptr_array) return false;
+    const int elt = r.dtype == 0 ? 4 : 8;
+    const int vw = 16 / elt, KU = vw, kc = 128 / elt;
+    const int tidx = r.transA * 2 + r.transB;
+    const int64_t M = r.M, N = r.N, K = r.K;
+    const bool AK = r.transA == 1, BK = r.transB == 0;
+    const int64_t rowsA = AK ? K : M, colsA = AK ? M : K, rowsB = BK ? K : N, colsB = BK ? N : K;
+    auto al16 = [&](int64_t el) { return (el * elt) % 16 == 0; };
+    if (r.align % 16 != 0 || !al16(r.lda) || !al16(r.ldb) || M > 256 || N > 256 || K < 1) return false;
+    if (r.batch > 1) {
+        if (!al16(r.sA) || !al16(r.sB) || r.sA < r.lda * colsA || r.sB < r.ldb * colsB) return false;
+        if (r.sA * elt >= (int64_t)1 << 40 || r.sB * elt >= (int64_t)1 << 40) return false;
+    }
+    if (r.batch >= ((int64_t)1 << 31)) return false;
+    const int a_pitch = AK ? kc : (int)round_up(M, vw), b_pitch = BK ? kc : (int)round_up(N, vw);
+    if (a_pitch > 256 || b_pitch > 256) return false;
+    const bool c_vec = r.align % 16 == 0 && al16(r.ldc) && (r.batch <= 1 || al16(r.sC));
+    const double hbm_per_problem = (double)(M * K + K * N + M * N * (r.beta_zero ? 1 : 2)) * elt;
+    const int nchunks = (int)((K + kc - 1) / kc);
+
+    static const int kMaps[8] = {-2, -1, 1, 2, 4, 8, 16, 32};
+    auto msplits = splits((int)M, 8, vw);
+    auto nsplits = splits((int)N, 8, vw);
+    KsCand best;
+    for (const auto &ms : msplits)
+        for (const auto &ns : nsplits) {
+            if (kn.mr && (ms.s[0].size != kn.mr || ns.s[0].size != kn.nr)) continue;
+            struct Cl {
+                int mr, nr, tm, tn, rb, cb;
+                double instr[8], wf[8];
+                bool ok[8];
+            } cl[4];
+            int ncl = 0;
+            bool avail = true;
+            int64_t memops = 2 * M * N;
+            int rb = 0;
+            for (int a = 0; a < ms.n && avail; ++a) {
+                int cb = 0;
+                for (int b = 0; b < ns.n; ++b) {
+                    const int mr = ms.s[a].size, nr = ns.s[b].size;
+                    if (!catalog_has(r.dtype, tidx, IAAT_FAM_KS_FMA, mr, nr)) {
+                        avail = false;
+                        break;
+                    }
+                    Cl &q = cl[ncl++];
+                    q.mr = mr;
+                    q.nr = nr;
+                    q.tm = ms.s[a].count;
+                    q.tn = ns.s[b].count;
+                    q.rb = rb;
+                    q.cb = cb;
+                    for (int m = 0; m < 8; ++m) {
+                        const int map = kMaps[m];
+                        q.ok[m] = true;
+                        if (kn.order >= 0 && !((kn.order == 0 && map == -2) || (kn.order == 1 && map == -1) ||
+                                               (kn.order >= 2 && map == kn.order - 1)))
+                            q.ok[m] = false;
+                        Lanes L = lane_map(map, q.tm * q.tn, q.tm, q.tn);
+                        if (map > 0 && (L.active < 24 || q.tm * q.tn < 32)) q.ok[m] = false;
+                        if (!q.ok[m]) continue;
+                        ks_class_cost(r, elt, mr, nr, L, rb, cb, q.tm, q.tn, a_pitch, b_pitch, kc, q.instr[m],
+                                      q.wf[m]);
+                    }
+                    memops += (int64_t)q.tm * q.tn * (mr + nr) * K;
+                    cb += ns.s[b].size * ns.s[b].count;
+                }
+                rb += ms.s[a].size * ms.s[a].count;
+            }
+            if (!avail) continue;
+            for (int ctas = 1; ctas <= 3; ++ctas) {
+                if (kn.ctas && ctas != kn.ctas) continue;
+                const int wmax = IAAT_MAX_THREADS / 32 / ctas - 1;
+                const int smem_cta = (int)std::min<int64_t>(IAAT_SMEM_LIMIT, 228 * 1024 / ctas - 1024);
+                for (int P = 1; P <= 64; ++P) {
+                    if (kn.p && P != kn.p) continue;
+                    if (P > 1 && (int64_t)(P - 1) * r.sm_count * ctas >= r.batch) break;
+                    int W = 0;
+                    double instr = 0, wf = 0;
+                    int pick[4];
+                    bool fits = true;
+                    for (int q = 0; q < ncl; ++q) {
+                        double bk = 1e300;
+                        pick[q] = -1;
+                        for (int m = 0; m < 8; ++m) {
+                            if (!cl[q].ok[m]) continue;
+                            const int w = class_warps(kMaps[m], P, cl[q].tm * cl[q].tn, cl[q].tm, cl[q].tn);
+                            const double k = w * std::max(cl[q].instr[m] / kIssuePerClk, cl[q].wf[m] / kSmemPerClk);
+                            if (k < bk * 0.999) {
+                                bk = k;
+                                pick[q] = m;
+                            }
+                        }
+                        if (pick[q] < 0) {
+                            fits = false;
+                            break;
+                        }
+                        const int w = class_warps(kMaps[pick[q]], P, cl[q].tm * cl[q].tn, cl[q].tm, cl[q].tn);
+                        W += w;
+                        instr += w * cl[q].instr[pick[q]];
+                        wf += w * cl[q].wf[pick[q]];
+                    }
+                    if (!fits) continue;
+                    if (W > wmax) break;
+                    const int a_bytes = (int)round_up((int64_t)P * (AK ? M * 128 : (int64_t)kc * a_pitch * elt), 1024);
+                    const int b_bytes = (int)round_up((int64_t)P * (BK ? N * 128 : (int64_t)kc * b_pitch * elt), 1024);
+                    const int stage = a_bytes + b_bytes;
+                    int S = std::min(IAAT_KS_MAX_STAGES, (smem_cta - IAAT_KS_BAR_BYTES - 1024) / stage);
+                    if (kn.s > 0) S = std::min(S, kn.s);
+                    if (S < 2) continue;
+                    // one round: every resident CTA finishes one unit
+                    const double nblk = (double)K / KU;
+                    const double t_hbm = ctas * P * hbm_per_problem / kHbmBytesPerClk;
+                    const double rate = std::min(kIssuePerClk, kIssuePerWarp * 1.5 * ctas * W);
+                    const double epi = (double)P * M * N * (r.beta_zero ? 2 : 4) / 32.0;
+                    const double t_issue = ctas * (instr * nblk + epi + W * nchunks * 12.0) / rate;
+                    const double t_smem = ctas * wf * nblk / kSmemPerClk;
+                    const double t_comp = std::max(t_issue, t_smem);
+                    // latency to fill: S stages must cover ~kLoadLatency of the ring
+                    const double t_lat = kLoadLatency * nchunks / std::max(1, S - 1) / ctas;
+                    const double t = std::max(std::max(t_hbm, t_comp), t_lat) + 0.15 * std::min(t_hbm, t_comp) + 300.0;
+                    const int64_t nunits = (r.batch + P - 1) / P;
+                    const int64_t slots = (int64_t)r.sm_count * ctas;
+                    const double total = t * (double)((nunits + slots - 1) / slots) + 3000.0;
+                    if (!(total < best.total * 0.995 || (!(best.total < total * 0.995) && memops < best.memops)))
+                        continue;
+                    KsCand c;
+                    c.ok = true;
+                    c.total = total;
+                    c.unit = t;
+                    c.P = P;
+                    c.S = S;
+                    c.W = W;
+                    c.ctas = ctas;
+                    c.a_bytes = a_bytes;
+                    c.b_bytes = b_bytes;
+                    c.a_pitch = a_pitch;
+                    c.b_pitch = b_pitch;
+                    c.ms = ms;
+                    c.ns = ns;
+                    c.memops = memops;
+                    c.ncls = ncl;
+                    int wb = 0;
+                    for (int q = 0; q < ncl; ++q) {
+                        const int map = kMaps[pick[q]];
+                        const int w = class_warps(map, P, cl[q].tm * cl[q].tn, cl[q].tm, cl[q].tn);
+                        c.cls[q] = IaatClass{catalog_code(IAAT_FAM_FMA, cl[q].mr, cl[q].nr), wb, wb + w,
+                                             cl[q].tm * cl[q].tn, cl[q].tm, cl[q].rb, cl[q].mr, cl[q].cb, cl[q].nr,
+                                             cl[q].tn, map == -1 ? 1 : 0, map > 0 ? map : 0};
+                        wb += w;
+                    }
+                    best = c;
+                }
+            }
+        }
+    if (!best.ok) return false;
+    Plan &pl = out;
+    pl = Plan();
+    pl.ks = 1;
+    IaatKsParams &k = pl.ksp;
+    std::memset(&k, 0, sizeof k);
+    k.sC = r.sC;
+    k.batch = r.batch;
+    k.nunits = (r.batch + best.P - 1) / best.P;
+    k.M = (int)M;
+    k.N = (int)N;
+    k.K = (int)K;
+    k.ldc = (int)r.ldc;
+    k.P = best.P;
+    k.S = best.S;
+    k.kc = kc;
+    k.nchunks = nchunks;
+    k.n_compute_warps = best.W;
+    k.a_pitch = best.a_pitch;
+    k.b_pitch = best.b_pitch;
+    k.a_bytes = best.a_bytes;
+    k.b_bytes = best.b_bytes;
+    k.a_tx = (int)((int64_t)best.P * (AK ? M * kc : (int64_t)kc * best.a_pitch) * elt);
+    k.b_tx = (int)((int64_t)best.P * (BK ? N * kc : (int64_t)kc * best.b_pitch) * elt);
+    k.stage_bytes = best.a_bytes + best.b_bytes;
+    k.beta_zero = r.beta_zero;
+    k.c_vec = c_vec ? 1 : 0;
+    k.nclasses = best.ncls;
+    for (int q = 0; q < best.ncls; ++q) k.cls[q] = best.cls[q];
+    auto geo = [&](TmaGeo &g, int64_t rows, int64_t cols, int64_t ld, int64_t stride, bool kmaj, int pitch, int D) {
+        g.dim[0] = (uint64_t)rows;
+        g.dim[1] = (uint64_t)cols;
+        g.dim[2] = (uint64_t)r.batch;
+        g.stride[0] = (uint64_t)(ld * elt);
+        g.stride[1] = (uint64_t)((r.batch > 1 ? stride : ld * cols) * elt);
+        if (kmaj) {
+            g.box[0] = (uint32_t)kc;
+            g.box[1] = (uint32_t)D;
+        } else {
+            g.box[0] = (uint32_t)pitch;
+            g.box[1] = (uint32_t)kc;
+        }
+        g.box[2] = (uint32_t)best.P;
+        g.swizzle128 = kmaj ? 1 : 0;
+    };
+    geo(pl.tmA, rowsA, colsA, r.lda, r.sA, AK, best.a_pitch, (int)M);
+    geo(pl.tmB, rowsB, colsB, r.ldb, r.sB, BK, best.b_pitch, (int)N);
+    pl.family = IAAT_FAM_KS_FMA;
+    pl.vec = 1;
+    pl.ctas = best.ctas;
+    pl.grid = (int)std::min<int64_t>(k.nunits, (int64_t)r.sm_count * best.ctas);
+    pl.block = (best.W + 1) * 32;
+    pl.smem = IAAT_KS_BAR_BYTES + 1024 + best.S * k.stage_bytes;
+    pl.nm = best.ms.n;
+    pl.nn = best.ns.n;
+    for (int i = 0; i < 2; ++i) {
+        pl.mstrip[i] = best.ms.s[i];
+        pl.nstrip[i] = best.ns.s[i];
+    }
+    pl.memops = best.memops;
+    pl.est_cycles = best.unit;
+    pl.est_total = best.total;
+    pl.status = 0;
+    return true;
+}
+
 std::string plan_json(const PlanRequest &r, const Plan &p)
 {
     char buf[512];
@@ -757,22 +1051,34 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
     }
     const IaatKParams &k = p.kp;
     add("\"tuned\": %d, ", p.tuned);
-    add("\"family\": \"%s\", \"vec\": %d, \"P\": %d, \"S\": %d, \"compute_warps\": %d, \"ctas_per_sm\": %d, "
-        "\"grid\": %d, \"block\": %d, \"smem\": %d, \"ngroups\": %lld, ",
-        p.family == IAAT_FAM_DMMA ? "dmma" : "fma", p.vec, k.P, k.S, k.n_compute_warps, p.ctas, p.grid, p.block,
-        p.smem, (long long)k.ngroups);
-    add("\"stage_a\": \"%s\", \"stage_b\": \"%s\", \"stage_c\": \"%s\", \"cap_a\": %d, \"cap_b\": %d, "
-        "\"cap_c\": %d, \"c_in_smem\": %d, \"prefetch_c\": %d, ",
-        k.modeA ? "perprob" : "slab", k.modeB ? "perprob" : "slab", k.modeC ? "perprob" : "slab", k.capA, k.capB,
-        k.capC, k.c_in_smem, k.prefetch_c);
+    const int ncls = p.ks ? p.ksp.nclasses : k.nclasses;
+    const IaatClass *cls = p.ks ? p.ksp.cls : k.cls;
+    if (p.ks) {
+        const IaatKsParams &q = p.ksp;
+        add("\"family\": \"ks_fma\", \"vec\": %d, \"P\": %d, \"S\": %d, \"compute_warps\": %d, "
+            "\"ctas_per_sm\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, \"ngroups\": %lld, ",
+            p.vec, q.P, q.S, q.n_compute_warps, p.ctas, p.grid, p.block, p.smem, (long long)q.nunits);
+        add("\"kc\": %d, \"nchunks\": %d, \"a_bytes\": %d, \"b_bytes\": %d, \"a_pitch\": %d, \"b_pitch\": %d, "
+            "\"a_swizzle128\": %d, \"b_swizzle128\": %d, \"c_vec\": %d, ",
+            q.kc, q.nchunks, q.a_bytes, q.b_bytes, q.a_pitch, q.b_pitch, p.tmA.swizzle128, p.tmB.swizzle128, q.c_vec);
+    } else {
+        add("\"family\": \"%s\", \"vec\": %d, \"P\": %d, \"S\": %d, \"compute_warps\": %d, \"ctas_per_sm\": %d, "
+            "\"grid\": %d, \"block\": %d, \"smem\": %d, \"ngroups\": %lld, ",
+            p.family == IAAT_FAM_DMMA ? "dmma" : "fma", p.vec, k.P, k.S, k.n_compute_warps, p.ctas, p.grid, p.block,
+            p.smem, (long long)k.ngroups);
+        add("\"stage_a\": \"%s\", \"stage_b\": \"%s\", \"stage_c\": \"%s\", \"cap_a\": %d, \"cap_b\": %d, "
+            "\"cap_c\": %d, \"c_in_smem\": %d, \"prefetch_c\": %d, ",
+            k.modeA ? "perprob" : "slab", k.modeB ? "perprob" : "slab", k.modeC ? "perprob" : "slab", k.capA,
+            k.capB, k.capC, k.c_in_smem, k.prefetch_c);
+    }
     add("\"m_strips\": [");
     for (int i = 0; i < p.nm; ++i) add("%s[%d, %d]", i ? ", " : "", p.mstrip[i].size, p.mstrip[i].count);
     add("], \"n_strips\": [");
     for (int i = 0; i < p.nn; ++i) add("%s[%d, %d]", i ? ", " : "", p.nstrip[i].size, p.nstrip[i].count);
     add("], \"memops\": %lld, \"est_cycles_per_group\": %.1f, \"est_cycles_total\": %.1f, \"classes\": [",
         (long long)p.memops, p.est_cycles, p.est_total);
-    for (int q = 0; q < k.nclasses; ++q) {
-        const IaatClass &c = k.cls[q];
+    for (int q = 0; q < ncls; ++q) {
+        const IaatClass &c = cls[q];
         add("%s{\"code\": %d, \"mr\": %d, \"nr\": %d, \"tiles\": %d, \"tm\": %d, \"row_base\": %d, "
             "\"col_base\": %d, \"warp_begin\": %d, \"warp_end\": %d, \"colfast\": %d, \"bm\": %d}",
             q ? ", " : "", c.code, c.mr, c.nr, c.tiles, c.tm, c.row_base, c.col_base, c.warp_begin,

@@ -28,9 +28,21 @@ struct Strip {
     int count;
 };
 
+// Geometry of one operand's 3-D TMA tensor map (K-streamed family); the
+// base address is bound at call time.
+struct TmaGeo {
+    uint64_t dim[3];      // elements: stored rows, stored cols, batch
+    uint64_t stride[2];   // bytes: ld * elt, problem stride * elt
+    uint32_t box[3];      // box extents (elements)
+    int swizzle128;       // 1: CU_TENSOR_MAP_SWIZZLE_128B (K-major operand)
+};
+
 struct Plan {
     int status = 0;        // iaat_status_t (SUCCESS or NOT_SUPPORTED)
     IaatKParams kp{};      // pointers / alpha / beta filled at call time
+    int ks = 0;            // 1: K-streamed family (ksp + tmA/tmB are the plan)
+    IaatKsParams ksp{};
+    TmaGeo tmA{}, tmB{};
     int grid = 0, block = 0, smem = 0;
     int vec = 0;           // kernel variant: 16-byte vector paths enabled
     int family = 0;        // IAAT_FAM_FMA or IAAT_FAM_DMMA

@@ -95,6 +95,10 @@ def catalog():
             for mr, nr in fma_tiles(dt, tr):
                 ents.append({"family": "fma", "dtype": dt, "trans": tr, "mr": mr, "nr": nr,
                              "code": fma_code(mr, nr)})
+        for tr in TRANS:
+            for mr, nr in ks_fma_tiles(dt, tr):
+                ents.append({"family": "ks_fma", "dtype": dt, "trans": tr, "mr": mr, "nr": nr,
+                             "code": fma_code(mr, nr)})
         if dt == "f64":
             for tr in TRANS:
                 for wm, wn in dmma_tiles(tr):
@@ -163,6 +167,85 @@ cudaError_t launch_%(name)s(const IaatKParams &p, int grid, int block, int smem,
 """ % {"dt": dt, "tr": tr, "vec": vec, "inc": inc, "name": name, "cases": "\n".join(cases), "T": T}
 
 
+KS_BUDGET = {"f32": 100, "f64": 100}
+
+
+def ks_regs(dt, tr, mr, nr, unr=1):
+    """K-streamed FMA tile: accumulators + UNR k-blocks of KU-deep fragments
+    of both operands (the K-major operand is always read 16 B along k), plus
+    one swizzled row address per K-major row / column."""
+    words = 1 if dt == "f32" else 2
+    kmaj = (mr if tr[0] == "T" else 0) + (nr if tr[1] == "N" else 0)
+    return words * (mr * nr + unr * KU[dt] * (mr + nr)) + kmaj
+
+
+def ks_fma_tiles(dt, tr):
+    return [(mr, nr) for mr in range(1, MAX_MR + 1) for nr in range(1, MAX_NR + 1)
+            if ks_regs(dt, tr, mr, nr) <= KS_BUDGET[dt]]
+
+
+def ks_unroll(dt, tr, mr, nr):
+    return 2 if ks_regs(dt, tr, mr, nr, 2) <= KS_BUDGET[dt] else 1
+
+
+def ks_kernel_name(dt, tr):
+    return "iaat_ks_%s_%s" % (dt, tr)
+
+
+def gen_ks_kernel_file(dt, tr):
+    """K-streamed TMA family (csrc/iaat_ks.cuh): same exact FMA micro-tile
+    catalog, one kernel per (dtype, transposition)."""
+    T = DTYPES[dt]
+    ta = "true" if tr[0] == "T" else "false"
+    tb = "true" if tr[1] == "T" else "false"
+    name = ks_kernel_name(dt, tr)
+    cases = []
+    for mr, nr in ks_fma_tiles(dt, tr):
+        cases.append("        case %d: ks_fma_class_loop<%s, %s, %s, %d, %d, %d>(p, c, smem, full, empty, warp, lane); break;"
+                     % (fma_code(mr, nr), T, ta, tb, mr, nr, ks_unroll(dt, tr, mr, nr)))
+    return """// GENERATED by gen/generate.py -- do not edit.  K-streamed kernel array entry for
+// dtype=%(dt)s trans=%(tr)s (install-time stage, PAPER.md:74-105).
+#include "../iaat_ks.cuh"
+
+namespace iaat {
+namespace {
+struct Dispatch_%(name)s {
+    static __device__ __forceinline__ void run(const IaatKsParams &p, const IaatClass &c,
+                                               unsigned char *smem, uint64_t *full,
+                                               uint64_t *empty, int warp, int lane)
+    {
+        switch (c.code) {
+%(cases)s
+        default: __trap();
+        }
+    }
+};
+}  // namespace
+
+__global__ void __launch_bounds__(IAAT_MAX_THREADS, 1)
+%(name)s(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+         const __grid_constant__ IaatKsParams p)
+{
+    ks_kernel_body<%(T)s, %(ta)s, %(tb)s, Dispatch_%(name)s>(&tmA, &tmB, p);
+}
+
+cudaError_t launch_%(name)s(const CUtensorMap &tmA, const CUtensorMap &tmB, const IaatKsParams &p,
+                             int grid, int block, int smem, cudaStream_t s)
+{
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(%(name)s, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             IAAT_SMEM_LIMIT);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    %(name)s<<<grid, block, smem, s>>>(tmA, tmB, p);
+    return cudaGetLastError();
+}
+}  // namespace iaat
+""" % {"dt": dt, "tr": tr, "name": name, "cases": "\n".join(cases), "T": T, "ta": ta, "tb": tb}
+
+
 def gen_table():
     decl, rows = [], []
     for di, dt in enumerate(DTYPES):
@@ -176,10 +259,21 @@ def gen_table():
         for tr in TRANS:
             tb.append("{&launch_%s, &launch_%s}" % (kernel_name(dt, tr, 0), kernel_name(dt, tr, 1)))
         body.append("    {" + ", ".join(tb) + "}")
+    ks_decl, ks_body = [], []
+    for dt in DTYPES:
+        for tr in TRANS:
+            ks_decl.append("cudaError_t launch_%s(const CUtensorMap &, const CUtensorMap &, const IaatKsParams &, "
+                           "int, int, int, cudaStream_t);" % ks_kernel_name(dt, tr))
+        ks_body.append("    {" + ", ".join("&launch_%s" % ks_kernel_name(dt, tr) for tr in TRANS) + "}")
     return ("// GENERATED by gen/generate.py -- launch table [dtype][trans NN,NT,TN,TT][vec]\n"
             "namespace iaat {\n" + "\n".join(decl) +
             "\ntypedef cudaError_t (*LaunchFn)(const IaatKParams &, int, int, int, cudaStream_t);\n"
-            "static const LaunchFn kLaunch[2][4][2] = {\n" + ",\n".join(body) + "\n};\n}  // namespace iaat\n")
+            "static const LaunchFn kLaunch[2][4][2] = {\n" + ",\n".join(body) + "\n};\n" +
+            "\n".join(ks_decl) +
+            "\ntypedef cudaError_t (*KsLaunchFn)(const CUtensorMap &, const CUtensorMap &, const IaatKsParams &, "
+            "int, int, int, cudaStream_t);\n"
+            "static const KsLaunchFn kLaunchKs[2][4] = {\n" + ",\n".join(ks_body) + "\n};\n"
+            "}  // namespace iaat\n")
 
 
 def gen_catalog_inc(ents):
@@ -190,7 +284,7 @@ def gen_catalog_inc(ents):
              "struct IaatCatalogEntry { int family; int dtype; int trans; int mr; int nr; int code; };",
              "static const IaatCatalogEntry kCatalog[] = {"]
     for e in ents:
-        lines.append("    {%d, %d, %d, %d, %d, %d}," % (0 if e["family"] == "fma" else 1,
+        lines.append("    {%d, %d, %d, %d, %d, %d}," % ({"fma": 0, "dmma": 1, "ks_fma": 2, "ks_dmma": 3}[e["family"]],
                                                         0 if e["dtype"] == "f32" else 1,
                                                         TRANS.index(e["trans"]),
                                                         e["mr"], e["nr"], e["code"]))
@@ -224,6 +318,9 @@ def main(argv=None):
                 p = os.path.join(args.out, "k_%s_%s_v%d.cu" % (dt, tr, vec))
                 write_if_changed(p, gen_kernel_file(dt, tr, vec))
                 files.append(p)
+            p = os.path.join(args.out, "ks_%s_%s.cu" % (dt, tr))
+            write_if_changed(p, gen_ks_kernel_file(dt, tr))
+            files.append(p)
     return files
 
 
