@@ -280,6 +280,8 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
 
     if (plan.ks) {
         IaatKsParams kp = plan.ksp;
+        static const int ks_debug = std::getenv("IAAT_DEBUG_KS") ? std::atoi(std::getenv("IAAT_DEBUG_KS")) : 0;
+        kp.debug = ks_debug;
         kp.C = static_cast<char *>(C);
         kp.alpha = a;
         kp.beta = b;
@@ -288,7 +290,15 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
             g_last_cuda_error = (int)cudaErrorInvalidValue;
             return IAAT_ERROR_CUDA;
         }
-        cudaError_t e = kLaunchKs[r.dtype][ta * 2 + tb](tmA, tmB, kp, plan.grid, plan.block, plan.smem, s);
+        KsLaunchFn fn = kLaunchKs[r.dtype][ta * 2 + tb];
+        if (plan.single) {
+            fn = nullptr;
+            for (const Ks1Entry &e : kLaunchKs1)
+                if (e.dtype == r.dtype && e.trans == ta * 2 + tb && e.mr == kp.cls[0].mr && e.nr == kp.cls[0].nr)
+                    fn = e.fn;
+            if (!fn) return IAAT_ERROR_NOT_SUPPORTED;
+        }
+        cudaError_t e = fn(tmA, tmB, kp, plan.grid, plan.block, plan.smem, s);
         if (e != cudaSuccess) {
             g_last_cuda_error = (int)e;
             return IAAT_ERROR_CUDA;

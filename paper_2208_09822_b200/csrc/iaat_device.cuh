@@ -138,6 +138,35 @@ __device__ __forceinline__ void st_vec(T *p, const T *in)
     *reinterpret_cast<V *>(p) = v;
 }
 
+// Global-space streaming accesses for C (ld/st.global.cs): C is touched
+// once per call, so it should not displace operands in L2; the explicit
+// space also avoids generic LD/ST.
+__device__ __forceinline__ float ldg_cs(const float *p) { return __ldcs(p); }
+__device__ __forceinline__ double ldg_cs(const double *p) { return __ldcs(p); }
+__device__ __forceinline__ void stg_cs(float *p, float v) { __stcs(p, v); }
+__device__ __forceinline__ void stg_cs(double *p, double v) { __stcs(p, v); }
+
+template <typename T>
+__device__ __forceinline__ void ldg_vec_cs(const T *p, T *out)
+{
+    typedef typename VecOf<T>::type V;
+    V v = __ldcs(reinterpret_cast<const V *>(p));
+    const T *e = reinterpret_cast<const T *>(&v);
+#pragma unroll
+    for (int w = 0; w < VecOf<T>::W; ++w) out[w] = e[w];
+}
+
+template <typename T>
+__device__ __forceinline__ void stg_vec_cs(T *p, const T *in)
+{
+    typedef typename VecOf<T>::type V;
+    V v;
+    T *e = reinterpret_cast<T *>(&v);
+#pragma unroll
+    for (int w = 0; w < VecOf<T>::W; ++w) e[w] = in[w];
+    __stcs(reinterpret_cast<V *>(p), v);
+}
+
 __device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
@@ -367,38 +396,85 @@ __device__ __forceinline__ void fma_tile(T (&acc)[MR][NR], const T *__restrict__
 
 // C = alpha*acc + beta*C_in, written once per element, never past the tile.
 // Cin: where C_in is read (the staged smem copy, or C itself); same ldc.
+// Fused alpha/beta epilogue of one lane's MR x NR tile whose element (i, j)
+// is C(row0 + i*rs, col0 + j*cs) (column-major, ldc); C_in is read through
+// Cin with the same offsets (the staged smem copy, or C itself), never when
+// beta == 0.  VR: rows contiguous (rs == 1) and 16-byte vector accesses
+// legal.  Columns are processed in blocks whose C_in values fit ~32
+// registers; inside a block every C_in load is issued before the first
+// store (a load after a store through a possibly aliasing pointer could not
+// be hoisted), so their latencies overlap instead of serialising.
+template <typename T, int MR, int NR, bool VR, bool CIN_GLOBAL = false>
+__device__ __forceinline__ void epilogue_tile(T (&acc)[MR][NR], T *C, const T *Cin, int ldc, int row0, int rs,
+                                              int col0, int cs, T alpha, T beta, bool beta_zero)
+{
+    constexpr int W = VecOf<T>::W;
+    constexpr bool V = VR && (MR % W) == 0;
+    constexpr int JB0 = (32 / (int)(sizeof(T) / 4)) / MR;
+    constexpr int JB = JB0 < 1 ? 1 : (JB0 > NR ? NR : JB0);
+#pragma unroll
+    for (int j0 = 0; j0 < NR; j0 += JB) {
+        T o[MR][JB];
+        if (!beta_zero) {
+#pragma unroll
+            for (int jj = 0; jj < JB; ++jj) {
+                if (j0 + jj >= NR) break;
+                const T *ci_p = Cin + (int64_t)(col0 + (j0 + jj) * cs) * ldc + row0;
+                if (V) {
+#pragma unroll
+                    for (int q = 0; q < MR / W; ++q) {
+                        T t[W];
+                        if (CIN_GLOBAL)
+                            ldg_vec_cs<T>(ci_p + q * W, t);
+                        else
+                            ld_vec<T>(ci_p + q * W, t);
+#pragma unroll
+                        for (int w = 0; w < W; ++w) o[q * W + w][jj] = t[w];
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < MR; ++i) o[i][jj] = CIN_GLOBAL ? ldg_cs(ci_p + i * rs) : ci_p[i * rs];
+                }
+            }
+#pragma unroll
+            for (int jj = 0; jj < JB; ++jj) {
+                if (j0 + jj >= NR) break;
+#pragma unroll
+                for (int i = 0; i < MR; ++i) o[i][jj] = fma_rn(alpha, acc[i][j0 + jj], mul_rn(beta, o[i][jj]));
+            }
+        } else {
+#pragma unroll
+            for (int jj = 0; jj < JB; ++jj) {
+                if (j0 + jj >= NR) break;
+#pragma unroll
+                for (int i = 0; i < MR; ++i) o[i][jj] = mul_rn(alpha, acc[i][j0 + jj]);
+            }
+        }
+#pragma unroll
+        for (int jj = 0; jj < JB; ++jj) {
+            if (j0 + jj >= NR) break;
+            T *c = C + (int64_t)(col0 + (j0 + jj) * cs) * ldc + row0;
+            if (V) {
+#pragma unroll
+                for (int q = 0; q < MR / W; ++q) {
+                    T t[W];
+#pragma unroll
+                    for (int w = 0; w < W; ++w) t[w] = o[q * W + w][jj];
+                    stg_vec_cs<T>(c + q * W, t);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < MR; ++i) stg_cs(c + i * rs, o[i][jj]);
+            }
+        }
+    }
+}
+
 template <typename T, int MR, int NR, bool VEC>
 __device__ __forceinline__ void epilogue(T (&acc)[MR][NR], T *C, const T *Cin, int ldc, int row0,
                                          int col0, T alpha, T beta, bool beta_zero)
 {
-    constexpr int W = VecOf<T>::W;
-#pragma unroll
-    for (int j = 0; j < NR; ++j) {
-        T *c = C + row0 + (int64_t)(col0 + j) * ldc;
-        const T *ci_p = Cin + row0 + (int64_t)(col0 + j) * ldc;
-        if (VEC && (MR % W) == 0) {
-#pragma unroll
-            for (int q = 0; q < MR / W; ++q) {
-                T o[W];
-                if (beta_zero) {
-#pragma unroll
-                    for (int w = 0; w < W; ++w) o[w] = mul_rn(alpha, acc[q * W + w][j]);
-                } else {
-                    T ci[W];
-                    ld_vec<T>(ci_p + q * W, ci);
-#pragma unroll
-                    for (int w = 0; w < W; ++w) o[w] = fma_rn(alpha, acc[q * W + w][j], mul_rn(beta, ci[w]));
-                }
-                st_vec<T>(c + q * W, o);
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < MR; ++i) {
-                T o = beta_zero ? mul_rn(alpha, acc[i][j]) : fma_rn(alpha, acc[i][j], mul_rn(beta, ci_p[i]));
-                c[i] = o;
-            }
-        }
-    }
+    epilogue_tile<T, MR, NR, VEC>(acc, C, Cin, ldc, row0, 1, col0, 1, alpha, beta, beta_zero);
 }
 
 // One compute warp running FMA tile class `c` over all groups of this CTA.

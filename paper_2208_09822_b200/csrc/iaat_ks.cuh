@@ -78,7 +78,8 @@ __device__ void ks_producer(const IaatKsParams &p, const CUtensorMap *tmA, const
     const uint64_t pol = policy_evict_first();
     const uint32_t tx = (uint32_t)(p.a_tx + p.b_tx);
     unsigned char *ring = ks_ring(smem);
-    int it = 0;
+    int s = 0, it = 0;
+    uint32_t phase = 0;  // parity of the empty barrier to wait for
     for (int64_t u = blockIdx.x; u < p.nunits; u += gridDim.x) {
         const int b0 = (int)(u * p.P);
         if (!p.beta_zero) {
@@ -92,8 +93,8 @@ __device__ void ks_producer(const IaatKsParams &p, const CUtensorMap *tmA, const
             bulk_prefetch_l2(reinterpret_cast<const void *>(lo), (uint32_t)(hi - lo));
         }
         for (int c = 0; c < p.nchunks; ++c, ++it) {
-            const int s = it % p.S;
-            if (it >= p.S) mbar_wait(&empty[s], ((it / p.S) - 1) & 1);
+            if (it >= p.S && (p.debug & 4)) return;  // timing mode: fill the ring once, never refill
+            if (it >= p.S) mbar_wait(&empty[s], phase);
             unsigned char *st = ring + (size_t)s * p.stage_bytes;
             mbar_arrive_expect_tx(&full[s], tx);
             const int k0 = c * p.kc;
@@ -101,6 +102,10 @@ __device__ void ks_producer(const IaatKsParams &p, const CUtensorMap *tmA, const
             else    tma_load_3d(st, tmA, 0, k0, b0, &full[s], pol);                 // A: M x K, MN-major
             if (TB) tma_load_3d(st + p.a_bytes, tmB, 0, k0, b0, &full[s], pol);     // B: N x K, MN-major
             else    tma_load_3d(st + p.a_bytes, tmB, k0, 0, b0, &full[s], pol);     // B: K x N, K-major
+            if (++s == p.S) {
+                s = 0;
+                if (it >= 2 * p.S - 1) phase ^= 1u;  // lap L >= 1 waits for parity (L - 1) & 1
+            }
         }
     }
 }
@@ -110,53 +115,171 @@ __device__ void ks_producer(const IaatKsParams &p, const CUtensorMap *tmA, const
 // (r * 128) | ((q ^ (r & 7)) << 4) == ((r * 128) | ((r & 7) << 4)) ^ (q << 4).
 __device__ __forceinline__ uint32_t kmaj_row_base(int r_abs) { return ((uint32_t)r_abs << 7) | ((uint32_t)(r_abs & 7) << 4); }
 
-// One k-block (KU = 16 B / elt k-steps) of R elements along the tile dim.
-// f[kk][r]: operand value at (tile element r, k = kb + kk).
-template <typename T, bool KMAJ, int R, int NB>
-__device__ __forceinline__ void ks_load_block(T (&f)[16 / sizeof(T)][R], const unsigned char *st,
-                                              const uint32_t (&rb)[NB], uint32_t mn_off, int pitch_bytes,
-                                              int kb)
+// One k-step of an MN-major operand: R consecutive elements at byte offset
+// `off` of the stage region (16-byte vectors when R allows).
+template <typename T, int R>
+__device__ __forceinline__ void ks_load_mn(T (&f)[R], const unsigned char *st, uint32_t off)
 {
-    constexpr int KU = 16 / sizeof(T);
-    if (KMAJ) {
-        const uint32_t q = (uint32_t)(kb / KU) << 4;
+    constexpr int W = 16 / sizeof(T);
+    const T *row = reinterpret_cast<const T *>(st + off);
+    if ((R % W) == 0) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            T t[KU];
-            ld_vec<T>(reinterpret_cast<const T *>(st + (rb[r < NB ? r : 0] ^ q)), t);
-#pragma unroll
-            for (int kk = 0; kk < KU; ++kk) f[kk][r] = t[kk];
-        }
+        for (int v = 0; v < R / W; ++v) ld_vec<T>(row + v * W, &f[v * W]);
     } else {
-        constexpr int W = 16 / sizeof(T);
 #pragma unroll
-        for (int kk = 0; kk < KU; ++kk) {
-            const T *row = reinterpret_cast<const T *>(st + mn_off + (uint32_t)((kb + kk) * pitch_bytes));
-            if ((R % W) == 0) {
-#pragma unroll
-                for (int v = 0; v < R / W; ++v) ld_vec<T>(row + v * W, &f[kk][v * W]);
-            } else {
-#pragma unroll
-                for (int r = 0; r < R; ++r) f[kk][r] = row[r];
-            }
-        }
+        for (int r = 0; r < R; ++r) f[r] = row[r];
     }
 }
 
-// Single k-step (scalar) for a ragged chunk tail.
-template <typename T, bool KMAJ, int R, int NB>
-__device__ __forceinline__ void ks_load_one(T (&f)[R], const unsigned char *st, const uint32_t (&rb)[NB],
-                                            uint32_t mn_off, int pitch_bytes, int k)
+// ------------------------------------------------------------------ FMA k-block fragments
+// Fragments of one k-block (KU k-steps) of a lane's tile: K-major operands
+// for all KU k-steps (one 16-byte load per row / column), MN-major operands
+// for the block's first k-step only (the remaining KU-1 are loaded inside
+// ks_frag_fma, one k-step ahead of their FMAs).
+template <typename T, bool AK, bool BK, int MR, int NR>
+struct KsFrag {
+    static constexpr int KU = 16 / sizeof(T);
+    T ka[AK ? KU : 1][MR];
+    T kb[BK ? KU : 1][NR];
+    T ma[AK ? 1 : MR];
+    T mb[BK ? 1 : NR];
+};
+
+// Shared-memory addressing of one operand inside the current stage, as byte
+// offsets from the dynamic smem base.
+//   K-major (swizzled rows): element (r-th row of the lane, k) lives at
+//       (base[r] ^ ((k / KU) << 4)) + (k % KU) * elt,  base[r] = stage + row_r*128 | (row_r & 7) << 4
+//     UNI: every row of the lane has the same swizzle phase (row stride a
+//       multiple of 8), so one XOR serves all rows: (base[0] ^ q) + r * rstride.
+//   MN-major: element (tile element r, k) at mn + k * pitch + r * elt.
+template <bool KMAJ, bool UNI, int R>
+struct KsOpnd {
+    uint32_t base[KMAJ && !UNI ? R : 1];
+    uint32_t rstride;  // UNI: byte stride between the lane's rows
+    uint32_t pitch;    // MN-major: bytes per k-step
+};
+
+template <typename T, bool KMAJ, bool UNI, int R>
+__device__ __forceinline__ void ks_ld_kblock(T (&f)[16 / sizeof(T)][R], const unsigned char *smem,
+                                             const KsOpnd<KMAJ, UNI, R> &o, int kb)
 {
     constexpr int KU = 16 / sizeof(T);
-    if (KMAJ) {
-        const uint32_t q = (uint32_t)(k / KU) << 4, w = (uint32_t)(k % KU) * sizeof(T);
+    const uint32_t q = (uint32_t)(kb / KU) << 4;
+    const uint32_t x0 = o.base[0] ^ q;
 #pragma unroll
-        for (int r = 0; r < R; ++r) f[r] = *reinterpret_cast<const T *>(st + ((rb[r < NB ? r : 0] ^ q) + w));
+    for (int r = 0; r < R; ++r) {
+        T t[KU];
+        const uint32_t off = UNI ? x0 + (uint32_t)r * o.rstride : (o.base[UNI ? 0 : r] ^ q);
+        ld_vec<T>(reinterpret_cast<const T *>(smem + off), t);
+#pragma unroll
+        for (int kk = 0; kk < KU; ++kk) f[kk][r] = t[kk];
+    }
+}
+
+template <typename T, bool AK, bool BK, bool UA, bool UB, int MR, int NR>
+__device__ __forceinline__ void ks_frag_load(KsFrag<T, AK, BK, MR, NR> &f, const unsigned char *smem,
+                                             const KsOpnd<AK, UA, MR> &oa, const KsOpnd<BK, UB, NR> &ob,
+                                             uint32_t a_mn, uint32_t b_mn, int kb)
+{
+    constexpr int KU = 16 / sizeof(T);
+    if (AK) ks_ld_kblock<T, AK, UA, MR>(reinterpret_cast<T (&)[KU][MR]>(f.ka), smem, oa, kb);
+    else ks_load_mn<T, MR>(reinterpret_cast<T (&)[MR]>(f.ma), smem, a_mn + (uint32_t)kb * oa.pitch);
+    if (BK) ks_ld_kblock<T, BK, UB, NR>(reinterpret_cast<T (&)[KU][NR]>(f.kb), smem, ob, kb);
+    else ks_load_mn<T, NR>(reinterpret_cast<T (&)[NR]>(f.mb), smem, b_mn + (uint32_t)kb * ob.pitch);
+}
+
+// acc(i,j) += sum over the KU k-steps of the block, k ascending, one FMA each.
+template <typename T, bool AK, bool BK, bool UA, bool UB, int MR, int NR>
+__device__ __forceinline__ void ks_frag_fma(T (&acc)[MR][NR], const KsFrag<T, AK, BK, MR, NR> &f,
+                                            const unsigned char *smem, const KsOpnd<AK, UA, MR> &oa,
+                                            const KsOpnd<BK, UB, NR> &ob, uint32_t a_mn, uint32_t b_mn, int kb)
+{
+    constexpr int KU = 16 / sizeof(T);
+    T ma[2][AK ? 1 : MR], mb[2][BK ? 1 : NR];
+    const uint32_t a0 = a_mn + (uint32_t)kb * oa.pitch, b0 = b_mn + (uint32_t)kb * ob.pitch;
+#pragma unroll
+    for (int kk = 0; kk < KU; ++kk) {
+        if (kk + 1 < KU) {  // next k-step of the MN-major operands
+            if (!AK) ks_load_mn<T, MR>(reinterpret_cast<T (&)[MR]>(ma[(kk + 1) & 1]), smem,
+                                       a0 + (uint32_t)(kk + 1) * oa.pitch);
+            if (!BK) ks_load_mn<T, NR>(reinterpret_cast<T (&)[NR]>(mb[(kk + 1) & 1]), smem,
+                                       b0 + (uint32_t)(kk + 1) * ob.pitch);
+        }
+#pragma unroll
+        for (int j = 0; j < NR; ++j)
+#pragma unroll
+            for (int i = 0; i < MR; ++i) {
+                const T av = AK ? f.ka[AK ? kk : 0][i] : (kk == 0 ? f.ma[AK ? 0 : i] : ma[kk & 1][AK ? 0 : i]);
+                const T bv = BK ? f.kb[BK ? kk : 0][j] : (kk == 0 ? f.mb[BK ? 0 : j] : mb[kk & 1][BK ? 0 : j]);
+                acc[i][j] = fma_rn(av, bv, acc[i][j]);
+            }
+    }
+}
+
+// One K-chunk (kv valid k-steps) of the lane's tile.  sa / sb: byte offsets
+// of the stage's A / B regions from the smem base; ra / rb: the lane's
+// swizzled row / column bases inside a region (K-major operands), a_mn /
+// b_mn: the lane's first element inside a region (MN-major operands).
+template <typename T, bool AK, bool BK, bool UA, bool UB, int MR, int NR, int UNR, int NA, int NB>
+__device__ __forceinline__ void ks_chunk(T (&acc)[MR][NR], const unsigned char *smem, uint32_t sa, uint32_t sb,
+                                         const uint32_t (&ra)[NA], const uint32_t (&rb)[NB], uint32_t a_mn,
+                                         uint32_t b_mn, uint32_t a_pitch, uint32_t b_pitch, uint32_t a_rs,
+                                         uint32_t b_rs, int kv)
+{
+    constexpr int KU = 16 / sizeof(T);
+    KsOpnd<AK, UA, MR> oa;
+    KsOpnd<BK, UB, NR> ob;
+#pragma unroll
+    for (int i = 0; i < (AK && !UA ? MR : 1); ++i) oa.base[i] = sa + ra[i < NA ? i : 0];
+#pragma unroll
+    for (int j = 0; j < (BK && !UB ? NR : 1); ++j) ob.base[j] = sb + rb[j < NB ? j : 0];
+    oa.rstride = a_rs;
+    ob.rstride = b_rs;
+    oa.pitch = a_pitch;
+    ob.pitch = b_pitch;
+    const uint32_t am = sa + a_mn, bm = sb + b_mn;
+    const int kfull = kv & ~(KU - 1);
+    int kb = 0;
+    if (UNR >= 2) {
+        // register double buffering (the paper's ping-pang):
+        // the fragments of k-block kb+KU load while the FMAs of kb issue
+        KsFrag<T, AK, BK, MR, NR> f0, f1;
+        if (kfull > 0) ks_frag_load<T, AK, BK, UA, UB, MR, NR>(f0, smem, oa, ob, am, bm, 0);
+        for (; kb < kfull; kb += 2 * KU) {
+            if (kb + KU < kfull) ks_frag_load<T, AK, BK, UA, UB, MR, NR>(f1, smem, oa, ob, am, bm, kb + KU);
+            ks_frag_fma<T, AK, BK, UA, UB, MR, NR>(acc, f0, smem, oa, ob, am, bm, kb);
+            if (kb + KU >= kfull) {
+                kb += KU;
+                break;
+            }
+            if (kb + 2 * KU < kfull) ks_frag_load<T, AK, BK, UA, UB, MR, NR>(f0, smem, oa, ob, am, bm, kb + 2 * KU);
+            ks_frag_fma<T, AK, BK, UA, UB, MR, NR>(acc, f1, smem, oa, ob, am, bm, kb + KU);
+        }
     } else {
-        const T *row = reinterpret_cast<const T *>(st + mn_off + (uint32_t)(k * pitch_bytes));
+#pragma unroll 2
+        for (; kb < kfull; kb += KU) {
+            KsFrag<T, AK, BK, MR, NR> f0;
+            ks_frag_load<T, AK, BK, UA, UB, MR, NR>(f0, smem, oa, ob, am, bm, kb);
+            ks_frag_fma<T, AK, BK, UA, UB, MR, NR>(acc, f0, smem, oa, ob, am, bm, kb);
+        }
+    }
+    // ragged tail of the chunk (K % KU), one k-step at a time
+#pragma unroll 1
+    for (; kb < kv; ++kb) {
+        T a[MR], b[NR];
+        const uint32_t q = (uint32_t)(kb / KU) << 4, w = (uint32_t)(kb % KU) * sizeof(T);
 #pragma unroll
-        for (int r = 0; r < R; ++r) f[r] = row[r];
+        for (int i = 0; i < MR; ++i)
+            a[i] = AK ? *reinterpret_cast<const T *>(smem + ((UA ? (oa.base[0] ^ q) + i * a_rs : (oa.base[AK && !UA ? i : 0] ^ q)) + w))
+                      : *reinterpret_cast<const T *>(smem + am + (uint32_t)kb * a_pitch + i * sizeof(T));
+#pragma unroll
+        for (int j = 0; j < NR; ++j)
+            b[j] = BK ? *reinterpret_cast<const T *>(smem + ((UB ? (ob.base[0] ^ q) + j * b_rs : (ob.base[BK && !UB ? j : 0] ^ q)) + w))
+                      : *reinterpret_cast<const T *>(smem + bm + (uint32_t)kb * b_pitch + j * sizeof(T));
+#pragma unroll
+        for (int j = 0; j < NR; ++j)
+#pragma unroll
+            for (int i = 0; i < MR; ++i) acc[i][j] = fma_rn(a[i], b[j], acc[i][j]);
     }
 }
 
@@ -168,6 +291,15 @@ __device__ __forceinline__ void ks_fma_class_loop(const IaatKsParams &p, const I
     constexpr int KU = 16 / sizeof(T);
     constexpr bool AK = TA;   // op(A) K-major in smem
     constexpr bool BK = !TB;  // op(B) K-major in smem
+    // Parameters are read once into registers: the function is not inlined,
+    // p and c arrive as generic pointers, and a load through them after a
+    // store to C could not be hoisted by the compiler.
+    const int K = p.K, kc = p.kc, nchunks = p.nchunks, P = p.P, S = p.S, M = p.M, N = p.N, ldc = p.ldc;
+    const int stage_bytes = p.stage_bytes, a_bytes = p.a_bytes, dbg = p.debug;
+    const bool beta_zero = p.beta_zero != 0, c_vec = p.c_vec != 0;
+    const int64_t nunits = p.nunits, batch = p.batch;
+    char *const Cbase = p.C;
+    const int tm = c.tm, tn = c.tn;
     // lane -> (local problem, tile row, tile col)
     int pl, ti, tj;
     bool tile_ok = true;
@@ -175,17 +307,17 @@ __device__ __forceinline__ void ks_fma_class_loop(const IaatKsParams &p, const I
         const int idx = (warp - c.warp_begin) * 32 + lane;
         pl = idx / c.tiles;
         const int t = idx - pl * c.tiles;
-        ti = c.colfast ? t / c.tn : t % c.tm;
-        tj = c.colfast ? t % c.tn : t / c.tm;
+        ti = c.colfast ? t / tn : t % tm;
+        tj = c.colfast ? t % tn : t / tm;
     } else {
         const int bn = 32 / c.bm;
-        const int nbm = (c.tm + c.bm - 1) / c.bm, nbn = (c.tn + bn - 1) / bn;
+        const int nbm = (tm + c.bm - 1) / c.bm, nbn = (tn + bn - 1) / bn;
         const int wb = warp - c.warp_begin;
         pl = wb / (nbm * nbn);
         const int blk = wb - pl * (nbm * nbn);
         ti = (blk % nbm) * c.bm + lane % c.bm;
         tj = (blk / nbm) * bn + lane / c.bm;
-        tile_ok = ti < c.tm && tj < c.tn;
+        tile_ok = ti < tm && tj < tn;
     }
     if (!tile_ok) {
         ti = 0;
@@ -196,99 +328,77 @@ __device__ __forceinline__ void ks_fma_class_loop(const IaatKsParams &p, const I
     const int row0 = AK ? c.row_base + ti : c.row_base + ti * MR;
     const int col0 = BK ? c.col_base + tj : c.col_base + tj * NR;
     // smem addressing inside a stage (problem pl of the unit)
-    const int pc = min(pl, p.P - 1);
+    const int pc = min(pl, P - 1);
     uint32_t ra[AK ? MR : 1], rbB[BK ? NR : 1];
 #pragma unroll
-    for (int i = 0; i < (AK ? MR : 1); ++i) ra[i] = kmaj_row_base(pc * p.M + row0 + c.tm * i);
+    for (int i = 0; i < (AK ? MR : 1); ++i) ra[i] = kmaj_row_base(pc * M + row0 + tm * i);
 #pragma unroll
-    for (int j = 0; j < (BK ? NR : 1); ++j) rbB[j] = kmaj_row_base(pc * p.N + col0 + c.tn * j);
-    const uint32_t a_mn = AK ? 0u : (uint32_t)((pc * p.kc * p.a_pitch + row0) * (int)sizeof(T));
-    const uint32_t b_mn = BK ? 0u : (uint32_t)((pc * p.kc * p.b_pitch + col0) * (int)sizeof(T));
-    const int a_pb = p.a_pitch * (int)sizeof(T), b_pb = p.b_pitch * (int)sizeof(T);
+    for (int j = 0; j < (BK ? NR : 1); ++j) rbB[j] = kmaj_row_base(pc * N + col0 + tn * j);
+    const uint32_t a_mn = AK ? 0u : (uint32_t)((pc * kc * p.a_pitch + row0) * (int)sizeof(T));
+    const uint32_t b_mn = BK ? 0u : (uint32_t)((pc * kc * p.b_pitch + col0) * (int)sizeof(T));
+    const uint32_t a_pb = (uint32_t)(p.a_pitch * (int)sizeof(T)), b_pb = (uint32_t)(p.b_pitch * (int)sizeof(T));
+    // uniform swizzle phase across the lane's rows / columns (row stride tm
+    // or tn a multiple of 8): one XOR per k-block instead of one per row
+    const bool ua = AK && (MR == 1 || (tm & 7) == 0), ub = BK && (NR == 1 || (tn & 7) == 0);
+    const uint32_t a_rs = (uint32_t)tm * 128u, b_rs = (uint32_t)tn * 128u;
+    const uint32_t ring_off = (uint32_t)(ks_ring(smem) - smem);
     const T alpha = (T)p.alpha, beta = (T)p.beta;
     const int64_t scb = p.sC * (int64_t)sizeof(T);
-    const unsigned char *ring = ks_ring(smem);
 
-    int it = 0;
-    for (int64_t u = blockIdx.x; u < p.nunits; u += gridDim.x) {
-        const int64_t b0 = u * p.P;
-        const bool active = tile_ok && (b0 + pl) < p.batch && pl < p.P;
+    int s = 0;
+    uint32_t phase = 0;
+    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int64_t b0 = u * P;
+        const bool active = tile_ok && (b0 + pl) < batch && pl < P;
         T acc[MR][NR];
 #pragma unroll
         for (int i = 0; i < MR; ++i)
 #pragma unroll
             for (int j = 0; j < NR; ++j) acc[i][j] = (T)0;
-        for (int ch = 0; ch < p.nchunks; ++ch, ++it) {
-            const int s = it % p.S;
-            mbar_wait(&full[s], (it / p.S) & 1);
-            if (active) {
-                const unsigned char *st = ring + (size_t)s * p.stage_bytes;
-                const unsigned char *sa = st, *sb = st + p.a_bytes;
-                const int kv = min(p.kc, p.K - ch * p.kc);
-                int kb = 0;
-#pragma unroll UNR
-                for (; kb + KU <= kv; kb += KU) {
-                    T a[KU][MR], b[KU][NR];
-                    ks_load_block<T, AK, MR>(a, sa, ra, a_mn, a_pb, kb);
-                    ks_load_block<T, BK, NR>(b, sb, rbB, b_mn, b_pb, kb);
-#pragma unroll
-                    for (int kk = 0; kk < KU; ++kk)
-#pragma unroll
-                        for (int j = 0; j < NR; ++j)
-#pragma unroll
-                            for (int i = 0; i < MR; ++i) acc[i][j] = fma_rn(a[kk][i], b[kk][j], acc[i][j]);
-                }
-#pragma unroll 1
-                for (; kb < kv; ++kb) {
-                    T a[MR], b[NR];
-                    ks_load_one<T, AK, MR>(a, sa, ra, a_mn, a_pb, kb);
-                    ks_load_one<T, BK, NR>(b, sb, rbB, b_mn, b_pb, kb);
-#pragma unroll
-                    for (int j = 0; j < NR; ++j)
-#pragma unroll
-                        for (int i = 0; i < MR; ++i) acc[i][j] = fma_rn(a[i], b[j], acc[i][j]);
-                }
+        for (int ch = 0; ch < nchunks; ++ch) {
+            if (!(dbg & 4)) mbar_wait(&full[s], phase);
+            if (active && !(dbg & 1)) {
+                const uint32_t sa = ring_off + (uint32_t)(s * stage_bytes), sb = sa + (uint32_t)a_bytes;
+                const int kv = min(kc, K - ch * kc);
+                // warp-uniform: one code path per swizzle-phase case
+                if (ua && ub)
+                    ks_chunk<T, AK, BK, AK, BK, MR, NR, UNR>(acc, smem, sa, sb, ra, rbB, a_mn, b_mn, a_pb, b_pb,
+                                                             a_rs, b_rs, kv);
+                else if (ua)
+                    ks_chunk<T, AK, BK, AK, false, MR, NR, UNR>(acc, smem, sa, sb, ra, rbB, a_mn, b_mn, a_pb, b_pb,
+                                                                a_rs, b_rs, kv);
+                else if (ub)
+                    ks_chunk<T, AK, BK, false, BK, MR, NR, UNR>(acc, smem, sa, sb, ra, rbB, a_mn, b_mn, a_pb, b_pb,
+                                                                a_rs, b_rs, kv);
+                else
+                    ks_chunk<T, AK, BK, false, false, MR, NR, UNR>(acc, smem, sa, sb, ra, rbB, a_mn, b_mn, a_pb,
+                                                                   b_pb, a_rs, b_rs, kv);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-        }
-        if (active) {
-            // fused epilogue: C = alpha*acc + beta*C_in (C_in never read when beta == 0)
-            T *C = reinterpret_cast<T *>(p.C + (b0 + pl) * scb);
-            constexpr int W = 16 / sizeof(T);
-#pragma unroll
-            for (int j = 0; j < NR; ++j) {
-                const int col = BK ? col0 + c.tn * j : col0 + j;
-                T *cc = C + (int64_t)col * p.ldc;
-                if (!AK && (MR % W) == 0 && p.c_vec) {
-#pragma unroll
-                    for (int v = 0; v < MR / W; ++v) {
-                        T o[W];
-                        if (p.beta_zero) {
-#pragma unroll
-                            for (int w = 0; w < W; ++w) o[w] = mul_rn(alpha, acc[v * W + w][j]);
-                        } else {
-                            T ci[W];
-                            ld_vec<T>(cc + row0 + v * W, ci);
-#pragma unroll
-                            for (int w = 0; w < W; ++w) o[w] = fma_rn(alpha, acc[v * W + w][j], mul_rn(beta, ci[w]));
-                        }
-                        st_vec<T>(cc + row0 + v * W, o);
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < MR; ++i) {
-                        T *q = cc + (AK ? row0 + c.tm * i : row0 + i);
-                        *q = p.beta_zero ? mul_rn(alpha, acc[i][j]) : fma_rn(alpha, acc[i][j], mul_rn(beta, *q));
-                    }
-                }
+            if (lane == 0 && !(dbg & 4)) mbar_arrive(&empty[s]);
+            if (++s == S) {
+                s = 0;
+                phase ^= 1u;
             }
+        }
+        if (active && !(dbg & 2)) {
+            // fused epilogue: C = alpha*acc + beta*C_in (C_in never read when beta == 0)
+            T *C = reinterpret_cast<T *>(Cbase + (b0 + pl) * scb);
+            if (!AK && c_vec)
+                epilogue_tile<T, MR, NR, true, true>(acc, C, C, ldc, row0, 1, col0, BK ? tn : 1, alpha, beta,
+                                                     beta_zero);
+            else
+                epilogue_tile<T, MR, NR, false, true>(acc, C, C, ldc, row0, AK ? tm : 1, col0, BK ? tn : 1, alpha,
+                                                      beta, beta_zero);
         }
     }
 }
 
 // ------------------------------------------------------------------ kernel body
-template <typename T, bool TA, bool TB, typename Dispatcher>
+// SINGLE: the plan has one tile class (single-class kernels) -- its fields
+// are then read straight from the constant bank instead of through a
+// dynamically indexed class table (registers).
+template <typename T, bool TA, bool TB, typename Dispatcher, bool SINGLE = false>
 __device__ __forceinline__ void ks_kernel_body(const CUtensorMap *tmA, const CUtensorMap *tmB,
                                                const IaatKsParams &p)
 {
@@ -306,6 +416,10 @@ __device__ __forceinline__ void ks_kernel_body(const CUtensorMap *tmA, const CUt
     __syncthreads();
     if (warp == p.n_compute_warps) {
         ks_producer<T, TA, TB>(p, tmA, tmB, smem, full, empty, lane);
+        return;
+    }
+    if (SINGLE) {
+        Dispatcher::run(p, p.cls[0], smem, full, empty, warp, lane);
         return;
     }
     int c = 0;

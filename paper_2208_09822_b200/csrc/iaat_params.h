@@ -25,6 +25,7 @@ enum IaatFamily : int {
     IAAT_FAM_DMMA = 1,    // per-warp (8*wm) x (8*wn) DMMA.8x8x4 tile (fp64 only, slab staging)
     IAAT_FAM_KS_FMA = 2,  // FMA tiles, K-streamed TMA staging (iaat_ks.cuh)
     IAAT_FAM_KS_DMMA = 3, // DMMA warp tiles, K-streamed TMA staging (fp64 only)
+    IAAT_FAM_KS1_FMA = 4, // single-class K-streamed kernels (one per tile; the big tiles)
 };
 
 // One tile class: all tiles of one exact size (mr x nr) inside one row strip
@@ -98,6 +99,7 @@ struct IaatKsParams {
     int stage_bytes;       // a_bytes + b_bytes
     int beta_zero;
     int c_vec;             // 16-byte C accesses legal (C base, ldc, stride aligned)
+    int debug;             // measurement only (IAAT_DEBUG_KS): bit0 skip the k loop, bit1 skip the epilogue, bit2 do not wait for data (timing only)
     int nclasses;
     IaatClass cls[IAAT_MAX_CLASSES];
 };

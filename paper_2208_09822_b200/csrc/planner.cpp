@@ -758,6 +758,7 @@ namespace {
 
 struct KsCand {
     bool ok = false;
+    int single = 0;
     double total = 1e300, unit = 0;
     int P = 0, S = 0, W = 0, ctas = 1, a_bytes = 0, b_bytes = 0, a_pitch = 0, b_pitch = 0;
     DimSplit ms, ns;
@@ -848,13 +849,17 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
             } cl[4];
             int ncl = 0;
             bool avail = true;
+            // one class covering C -> its single-class kernel if generated;
+            // otherwise every class must be in the multi-class kernel
+            const bool one = ms.n == 1 && ns.n == 1;
+            const int single = one && catalog_has(r.dtype, tidx, IAAT_FAM_KS1_FMA, ms.s[0].size, ns.s[0].size) ? 1 : 0;
             int64_t memops = 2 * M * N;
             int rb = 0;
             for (int a = 0; a < ms.n && avail; ++a) {
                 int cb = 0;
                 for (int b = 0; b < ns.n; ++b) {
                     const int mr = ms.s[a].size, nr = ns.s[b].size;
-                    if (!catalog_has(r.dtype, tidx, IAAT_FAM_KS_FMA, mr, nr)) {
+                    if (!single && !catalog_has(r.dtype, tidx, IAAT_FAM_KS_FMA, mr, nr)) {
                         avail = false;
                         break;
                     }
@@ -941,6 +946,7 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
                         continue;
                     KsCand c;
                     c.ok = true;
+                    c.single = single;
                     c.total = total;
                     c.unit = t;
                     c.P = P;
@@ -1016,6 +1022,7 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
     geo(pl.tmA, rowsA, colsA, r.lda, r.sA, AK, best.a_pitch, (int)M);
     geo(pl.tmB, rowsB, colsB, r.ldb, r.sB, BK, best.b_pitch, (int)N);
     pl.family = IAAT_FAM_KS_FMA;
+    pl.single = best.single;
     pl.vec = 1;
     pl.ctas = best.ctas;
     pl.grid = (int)std::min<int64_t>(k.nunits, (int64_t)r.sm_count * best.ctas);
@@ -1055,9 +1062,10 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
     const IaatClass *cls = p.ks ? p.ksp.cls : k.cls;
     if (p.ks) {
         const IaatKsParams &q = p.ksp;
-        add("\"family\": \"ks_fma\", \"vec\": %d, \"P\": %d, \"S\": %d, \"compute_warps\": %d, "
+        add("\"family\": \"%s\", \"vec\": %d, \"P\": %d, \"S\": %d, \"compute_warps\": %d, "
             "\"ctas_per_sm\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, \"ngroups\": %lld, ",
-            p.vec, q.P, q.S, q.n_compute_warps, p.ctas, p.grid, p.block, p.smem, (long long)q.nunits);
+            p.single ? "ks1_fma" : "ks_fma", p.vec, q.P, q.S, q.n_compute_warps, p.ctas, p.grid, p.block, p.smem,
+            (long long)q.nunits);
         add("\"kc\": %d, \"nchunks\": %d, \"a_bytes\": %d, \"b_bytes\": %d, \"a_pitch\": %d, \"b_pitch\": %d, "
             "\"a_swizzle128\": %d, \"b_swizzle128\": %d, \"c_vec\": %d, ",
             q.kc, q.nchunks, q.a_bytes, q.b_bytes, q.a_pitch, q.b_pitch, p.tmA.swizzle128, p.tmB.swizzle128, q.c_vec);

@@ -41,6 +41,7 @@ struct Plan {
     int status = 0;        // iaat_status_t (SUCCESS or NOT_SUPPORTED)
     IaatKParams kp{};      // pointers / alpha / beta filled at call time
     int ks = 0;            // 1: K-streamed family (ksp + tmA/tmB are the plan)
+    int single = 0;        // K-streamed: 1 = a single-class kernel (tile ksp.cls[0].mr x nr)
     IaatKsParams ksp{};
     TmaGeo tmA{}, tmB{};
     int grid = 0, block = 0, smem = 0;

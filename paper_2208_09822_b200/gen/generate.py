@@ -99,6 +99,9 @@ def catalog():
             for mr, nr in ks_fma_tiles(dt, tr):
                 ents.append({"family": "ks_fma", "dtype": dt, "trans": tr, "mr": mr, "nr": nr,
                              "code": fma_code(mr, nr)})
+            for mr, nr in ks1_tiles(dt, tr):
+                ents.append({"family": "ks1_fma", "dtype": dt, "trans": tr, "mr": mr, "nr": nr,
+                             "code": fma_code(mr, nr)})
         if dt == "f64":
             for tr in TRANS:
                 for wm, wn in dmma_tiles(tr):
@@ -167,42 +170,83 @@ cudaError_t launch_%(name)s(const IaatKParams &p, int grid, int block, int smem,
 """ % {"dt": dt, "tr": tr, "vec": vec, "inc": inc, "name": name, "cases": "\n".join(cases), "T": T}
 
 
-KS_BUDGET = {"f32": 100, "f64": 100}
-
-
-def ks_regs(dt, tr, mr, nr, unr=1):
-    """K-streamed FMA tile: accumulators + UNR k-blocks of KU-deep fragments
-    of both operands (the K-major operand is always read 16 B along k), plus
-    one swizzled row address per K-major row / column."""
-    words = 1 if dt == "f32" else 2
-    kmaj = (mr if tr[0] == "T" else 0) + (nr if tr[1] == "N" else 0)
-    return words * (mr * nr + unr * KU[dt] * (mr + nr)) + kmaj
-
-
 def ks_fma_tiles(dt, tr):
+    """K-streamed multi-class kernel (one warp-uniform switch over the tile
+    classes of a plan): the tiles whose inlined cases keep the whole kernel
+    spill-free under the 128-register bound (tests/test_build.py)."""
+    lim = KS_MULTI_MAX_AREA[dt]
     return [(mr, nr) for mr in range(1, MAX_MR + 1) for nr in range(1, MAX_NR + 1)
-            if ks_regs(dt, tr, mr, nr) <= KS_BUDGET[dt]]
+            if mr * nr <= lim and ks_unroll(dt, tr, mr, nr) > 0]
+
+
+def ks1_tiles(dt, tr):
+    return [t for t in KS1_TILES[dt] if ks_unroll(dt, tr, *t) > 0]
+
+
+KS_MULTI_MAX_AREA = {"f32": 24, "f64": 8}
+# single-class kernels (one exact tile class covers the whole C): each is its
+# own kernel, so each gets its own register allocation -- the big tiles live
+# here (tools/ks_regs.py checks them one by one)
+KS1_TILES = {
+    "f32": [(2, 4), (4, 2), (2, 8), (8, 2), (3, 8), (8, 3), (4, 4), (4, 5), (5, 4), (4, 6), (6, 4), (4, 7), (7, 4),
+            (4, 8), (8, 4), (5, 5), (5, 8), (8, 5), (6, 6), (6, 8), (8, 6), (7, 8), (8, 7), (8, 8)],
+    "f64": [(2, 2), (2, 4), (4, 2), (2, 8), (8, 2), (4, 4), (4, 8), (8, 4)],
+}
+
+
+_KS_UNROLL = None
 
 
 def ks_unroll(dt, tr, mr, nr):
-    return 2 if ks_regs(dt, tr, mr, nr, 2) <= KS_BUDGET[dt] else 1
+    """k-block register buffering of a K-streamed entry: 2 = double-buffered
+    (ping-pang, PAPER.md:181), 1 = single, 0 = spills even single-buffered
+    (entry left out).  Measured at install time by tools/ks_regs.py (ptxas
+    -v on one-entry kernels) into gen/ks_unroll.json -- the analogue of the
+    paper's register-allocator budget (PAPER.md:217-235)."""
+    global _KS_UNROLL
+    if _KS_UNROLL is None:
+        p = os.path.join(HERE, "ks_unroll.json")
+        _KS_UNROLL = json.load(open(p)) if os.path.exists(p) else {}
+    return _KS_UNROLL.get("%s_%s_%dx%d" % (dt, tr, mr, nr), 1)
 
 
 def ks_kernel_name(dt, tr):
     return "iaat_ks_%s_%s" % (dt, tr)
 
 
+def ks1_kernel_name(dt, tr, mr, nr):
+    return "iaat_ks1_%s_%s_%dx%d" % (dt, tr, mr, nr)
+
+
+KS_LAUNCH = """
+cudaError_t launch_%(name)s(const CUtensorMap &tmA, const CUtensorMap &tmB, const IaatKsParams &p,
+                             int grid, int block, int smem, cudaStream_t s)
+{
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(%(name)s, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             IAAT_SMEM_LIMIT);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    %(name)s<<<grid, block, smem, s>>>(tmA, tmB, p);
+    return cudaGetLastError();
+}
+"""
+
+
 def gen_ks_kernel_file(dt, tr):
-    """K-streamed TMA family (csrc/iaat_ks.cuh): same exact FMA micro-tile
-    catalog, one kernel per (dtype, transposition)."""
+    """K-streamed TMA family (csrc/iaat_ks.cuh): the multi-class kernel of
+    one (dtype, transposition)."""
     T = DTYPES[dt]
     ta = "true" if tr[0] == "T" else "false"
     tb = "true" if tr[1] == "T" else "false"
     name = ks_kernel_name(dt, tr)
     cases = []
     for mr, nr in ks_fma_tiles(dt, tr):
-        cases.append("        case %d: ks_fma_class_loop<%s, %s, %s, %d, %d, %d>(p, c, smem, full, empty, warp, lane); break;"
-                     % (fma_code(mr, nr), T, ta, tb, mr, nr, ks_unroll(dt, tr, mr, nr)))
+        # single-buffered here: the union of the inlined cases is what ptxas allocates
+        cases.append("        case %d: ks_fma_class_loop<%s, %s, %s, %d, %d, 1>(p, c, smem, full, empty, warp, lane); break;"
+                     % (fma_code(mr, nr), T, ta, tb, mr, nr))
     return """// GENERATED by gen/generate.py -- do not edit.  K-streamed kernel array entry for
 // dtype=%(dt)s trans=%(tr)s (install-time stage, PAPER.md:74-105).
 #include "../iaat_ks.cuh"
@@ -228,22 +272,46 @@ __global__ void __launch_bounds__(IAAT_MAX_THREADS, 1)
 {
     ks_kernel_body<%(T)s, %(ta)s, %(tb)s, Dispatch_%(name)s>(&tmA, &tmB, p);
 }
-
-cudaError_t launch_%(name)s(const CUtensorMap &tmA, const CUtensorMap &tmB, const IaatKsParams &p,
-                             int grid, int block, int smem, cudaStream_t s)
-{
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(%(name)s, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             IAAT_SMEM_LIMIT);
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
-    %(name)s<<<grid, block, smem, s>>>(tmA, tmB, p);
-    return cudaGetLastError();
-}
+%(launch)s
 }  // namespace iaat
-""" % {"dt": dt, "tr": tr, "name": name, "cases": "\n".join(cases), "T": T, "ta": ta, "tb": tb}
+""" % {"dt": dt, "tr": tr, "name": name, "cases": "\n".join(cases), "T": T, "ta": ta, "tb": tb,
+       "launch": KS_LAUNCH % {"name": name}}
+
+
+def gen_ks1_file(dt, tr):
+    """Single-class K-streamed kernels of one (dtype, transposition)."""
+    T = DTYPES[dt]
+    ta = "true" if tr[0] == "T" else "false"
+    tb = "true" if tr[1] == "T" else "false"
+    parts = []
+    for mr, nr in ks1_tiles(dt, tr):
+        name = ks1_kernel_name(dt, tr, mr, nr)
+        parts.append("""
+struct Dispatch_%(name)s {
+    static __device__ __forceinline__ void run(const IaatKsParams &p, const IaatClass &c,
+                                               unsigned char *smem, uint64_t *full,
+                                               uint64_t *empty, int warp, int lane)
+    {
+        ks_fma_class_loop<%(T)s, %(ta)s, %(tb)s, %(mr)d, %(nr)d, %(unr)d>(p, c, smem, full, empty, warp, lane);
+    }
+};
+
+__global__ void __launch_bounds__(IAAT_MAX_THREADS, 1)
+%(name)s(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+         const __grid_constant__ IaatKsParams p)
+{
+    ks_kernel_body<%(T)s, %(ta)s, %(tb)s, Dispatch_%(name)s, true>(&tmA, &tmB, p);
+}
+%(launch)s""" % {"name": name, "T": T, "ta": ta, "tb": tb, "mr": mr, "nr": nr, "launch": KS_LAUNCH % {"name": name},
+                     "unr": ks_unroll(dt, tr, mr, nr)})
+    return """// GENERATED by gen/generate.py -- do not edit.  Single-class K-streamed kernels,
+// dtype=%s trans=%s (install-time stage, PAPER.md:74-105).
+#include "../iaat_ks.cuh"
+
+namespace iaat {
+%s
+}  // namespace iaat
+""" % (dt, tr, "".join(parts))
 
 
 def gen_table():
@@ -259,11 +327,16 @@ def gen_table():
         for tr in TRANS:
             tb.append("{&launch_%s, &launch_%s}" % (kernel_name(dt, tr, 0), kernel_name(dt, tr, 1)))
         body.append("    {" + ", ".join(tb) + "}")
-    ks_decl, ks_body = [], []
+    ks_decl, ks_body, ks1 = [], [], []
     for dt in DTYPES:
         for tr in TRANS:
             ks_decl.append("cudaError_t launch_%s(const CUtensorMap &, const CUtensorMap &, const IaatKsParams &, "
                            "int, int, int, cudaStream_t);" % ks_kernel_name(dt, tr))
+            for mr, nr in ks1_tiles(dt, tr):
+                ks_decl.append("cudaError_t launch_%s(const CUtensorMap &, const CUtensorMap &, const IaatKsParams &, "
+                               "int, int, int, cudaStream_t);" % ks1_kernel_name(dt, tr, mr, nr))
+                ks1.append("    {%d, %d, %d, %d, &launch_%s}," % (list(DTYPES).index(dt), TRANS.index(tr), mr, nr,
+                                                                  ks1_kernel_name(dt, tr, mr, nr)))
         ks_body.append("    {" + ", ".join("&launch_%s" % ks_kernel_name(dt, tr) for tr in TRANS) + "}")
     return ("// GENERATED by gen/generate.py -- launch table [dtype][trans NN,NT,TN,TT][vec]\n"
             "namespace iaat {\n" + "\n".join(decl) +
@@ -273,6 +346,8 @@ def gen_table():
             "\ntypedef cudaError_t (*KsLaunchFn)(const CUtensorMap &, const CUtensorMap &, const IaatKsParams &, "
             "int, int, int, cudaStream_t);\n"
             "static const KsLaunchFn kLaunchKs[2][4] = {\n" + ",\n".join(ks_body) + "\n};\n"
+            "struct Ks1Entry { int dtype, trans, mr, nr; KsLaunchFn fn; };\n"
+            "static const Ks1Entry kLaunchKs1[] = {\n" + "\n".join(ks1) + "\n};\n"
             "}  // namespace iaat\n")
 
 
@@ -284,7 +359,7 @@ def gen_catalog_inc(ents):
              "struct IaatCatalogEntry { int family; int dtype; int trans; int mr; int nr; int code; };",
              "static const IaatCatalogEntry kCatalog[] = {"]
     for e in ents:
-        lines.append("    {%d, %d, %d, %d, %d, %d}," % ({"fma": 0, "dmma": 1, "ks_fma": 2, "ks_dmma": 3}[e["family"]],
+        lines.append("    {%d, %d, %d, %d, %d, %d}," % ({"fma": 0, "dmma": 1, "ks_fma": 2, "ks_dmma": 3, "ks1_fma": 4}[e["family"]],
                                                         0 if e["dtype"] == "f32" else 1,
                                                         TRANS.index(e["trans"]),
                                                         e["mr"], e["nr"], e["code"]))
@@ -320,6 +395,9 @@ def main(argv=None):
                 files.append(p)
             p = os.path.join(args.out, "ks_%s_%s.cu" % (dt, tr))
             write_if_changed(p, gen_ks_kernel_file(dt, tr))
+            files.append(p)
+            p = os.path.join(args.out, "ks1_%s_%s.cu" % (dt, tr))
+            write_if_changed(p, gen_ks1_file(dt, tr))
             files.append(p)
     return files
 

@@ -158,6 +158,8 @@ def tune_shape(sh, log):
             p = b.plan()
             if p["status"] != 0:
                 return None
+            if kw.get("family") == 2 and not p["family"].startswith("ks"):
+                return None  # K-streamed plan not applicable: the planner fell back
             us = b.time_us()
         except Exception:
             return None
@@ -176,13 +178,21 @@ def tune_shape(sh, log):
         for (wm, wn) in ((1, 1), (1, 2), (2, 1), (2, 2)):
             for P in Ps:
                 trial(tile="%dx%d" % (8 * wm, 8 * wn), p=P, family=1)
+    if max(M, N, K) >= 20:  # K-streamed TMA family (csrc/iaat_ks.cuh)
+        ks_tiles = [t for t in ("4x8", "8x4", "4x4", "6x8", "8x6", "5x8", "8x5", "4x6", "6x4", "2x8", "8x2")
+                    if int(t.split("x")[0]) <= M and int(t.split("x")[1]) <= N]
+        for tile in ks_tiles:
+            for order in (0, 1, 5, 9):
+                for P in (1, 2, 3):
+                    for ctas in (1, 2, 3):
+                        trial(family=2, tile=tile, order=order, p=P, ctas=ctas)
     if beta != 0:  # C_in from global (L2-prefetched) instead of staged: frees smem
         per_ab = (M * K + K * N) * elt
         for (mr, nr) in tile_options(M, N):
             for P in sorted({max(1, int(kb * 1024) // per_ab) for kb in (24, 48, 96)}):
                 trial(tile="%dx%d" % (mr, nr), p=P, csmem=0)
     results.sort(key=lambda x: x[0])
-    top = results[:4]
+    top = [r for r in results if r[1].get("family") != 2][:4]
     for us, kw, p in top:
         for order in (0, 1, 3, 5, 9, 17):
             for ctas in (1, 2, 3, 4):

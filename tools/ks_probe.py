@@ -46,13 +46,13 @@ def main():
         base = b.time_us()
         print("%s %s n=%d batch=%d: default plan %.1f us  plan=%s" % (dtype, tr, n, b.batch, base,
                                                                     b.plan()["family"]), flush=True)
-        tiles = ["4x8", "8x4", "4x4", "8x2", "2x8", "4x6", "6x4", "5x8", "8x5"]
-        for tile, order, P, ctas in itertools.product(tiles, (0, 1, 3, 5, 9, 17), (1, 2, 3), (1, 2, 3)):
+        tiles = ["4x8", "8x4", "4x4", "6x8", "8x6", "5x8", "8x5", "4x6", "6x4"]
+        for tile, order, P, ctas in itertools.product(tiles, (0, 1, 5, 9), (1, 2, 3), (1, 2, 3)):
             kw = dict(family=2, tile=tile, order=order, p=P, ctas=ctas)
             set_knobs(**kw)
             try:
                 p = b.plan()
-                if p["status"] != 0 or p["family"] != "ks_fma":
+                if p["status"] != 0 or not p["family"].startswith("ks"):
                     continue
                 key = (tile, p["classes"][0]["bm"], p["classes"][0]["colfast"], p["P"], p["ctas_per_sm"])
                 if any(r[2] == key for r in res):
