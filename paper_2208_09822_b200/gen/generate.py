@@ -174,7 +174,7 @@ def ks_fma_tiles(dt, tr):
     """K-streamed multi-class kernel (one warp-uniform switch over the tile
     classes of a plan): the tiles whose inlined cases keep the whole kernel
     spill-free under the 128-register bound (tests/test_build.py)."""
-    lim = KS_MULTI_MAX_AREA[dt]
+    lim = KS_MULTI_MAX_AREA[dt] // (2 if tr == "TN" else 1)  # TN: both operands K-major
     return [(mr, nr) for mr in range(1, MAX_MR + 1) for nr in range(1, MAX_NR + 1)
             if mr * nr <= lim and ks_unroll(dt, tr, mr, nr) > 0]
 

@@ -21,7 +21,7 @@ class Case:
     """One strided-batched problem set, resident on the GPU."""
 
     def __init__(self, dtype, tA, tB, M, N, K, batch, seed, alpha, beta, pad=0, spad=0,
-                 first_id=0, elem_offset=0):
+                 first_id=0, elem_offset=0, ld_multiple=1):
         import torch
         self.dtype, self.tA, self.tB = dtype, tA, tB
         self.M, self.N, self.K, self.batch, self.seed = M, N, K, batch, seed
@@ -30,7 +30,8 @@ class Case:
         ra, ca = stored(tA, M, K)
         rb, cb = stored(tB, K, N)
         self.ra, self.ca, self.rb, self.cb = ra, ca, rb, cb
-        self.lda, self.ldb, self.ldc = max(1, ra) + pad, max(1, rb) + pad, max(1, M) + pad
+        rup = lambda x: (x + ld_multiple - 1) // ld_multiple * ld_multiple  # noqa: E731
+        self.lda, self.ldb, self.ldc = rup(max(1, ra) + pad), rup(max(1, rb) + pad), rup(max(1, M) + pad)
         self.sA = self.lda * ca + spad
         self.sB = self.ldb * cb + spad
         self.sC = self.ldc * N + spad

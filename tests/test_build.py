@@ -17,14 +17,26 @@ LIB = os.path.join(ROOT, "paper_2208_09822_b200", "libiaat.so")
 
 
 def test_no_spills_in_any_kernel():
-    logs = glob.glob(os.path.join(BUILD, "ptxas_k_*.log"))
+    logs = glob.glob(os.path.join(BUILD, "ptxas_k_*.log")) + glob.glob(os.path.join(BUILD, "ptxas_ks1_*.log"))
     if not logs:
         pytest.skip("no ptxas logs (library built elsewhere)")
     for lg in logs:
         txt = open(lg).read()
         for m in re.finditer(r"(\d+) bytes spill stores, (\d+) bytes spill loads", txt):
-            assert m.group(1) == "0" and m.group(2) == "0", lg
+            # K-streamed single-class entries may keep a few words outside the
+            # k loop (the install-time check admits <= 64 B, tools/ks_regs.py)
+            lim = 64 if "ptxas_ks1_" in lg else 0
+            assert int(m.group(1)) <= lim and int(m.group(2)) <= 4 * lim, lg
         assert "Used" in txt
+
+
+def test_multiclass_ks_kernels_spill_little():
+    logs = glob.glob(os.path.join(BUILD, "ptxas_ks_*.log"))
+    if not logs:
+        pytest.skip("no ptxas logs (library built elsewhere)")
+    for lg in logs:
+        for m in re.finditer(r"(\d+) bytes spill stores, (\d+) bytes spill loads", open(lg).read()):
+            assert int(m.group(1)) <= 64, lg
 
 
 @functools.lru_cache(maxsize=1)
@@ -37,6 +49,7 @@ def _sass():
 def test_sass_has_bulk_copies_mbarriers_dmma():
     sass = _sass()
     assert "UBLKCP" in sass, "cp.async.bulk staging missing"
+    assert "UTMALDG" in sass, "TMA tensor-map staging (K-streamed family) missing"
     assert "SYNCS" in sass, "mbarrier ops missing"
     assert "DMMA" in sass, "fp64 DMMA tensor-core path missing"
     assert "FFMA" in sass and "DFMA" in sass
@@ -47,7 +60,7 @@ def test_fp32_kernels_use_no_tensor_cores():
     sass = _sass()
     # split per function; fp32 kernels must not contain HMMA (TF32/F16 MMAs)
     funcs = re.split(r"\n\s*Function : ", sass)
-    f32 = [f for f in funcs if "iaat_f32" in f.split("\n", 1)[0]]
+    f32 = [f for f in funcs if "_f32" in f.split("\n", 1)[0] and "iaat" in f.split("\n", 1)[0]]
     assert f32
     for f in f32:
         assert "HMMA" not in f and "UTCHMMA" not in f and "DMMA" not in f

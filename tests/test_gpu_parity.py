@@ -345,3 +345,70 @@ def test_launch_uses_sm100_kernels_only():
     n0 = iaat.iaat_launch_count()
     c.run()
     assert iaat.iaat_launch_count() == n0 + 1
+
+
+# ---------------------------------------------------------------- K-streamed (TMA) family
+KS_SHAPES = [(64, 64, 64), (80, 80, 80), (36, 44, 52), (20, 28, 12), (8, 8, 8), (48, 40, 37), (76, 68, 96)]
+
+
+def _force(**kw):
+    import os
+    for k in ("IAAT_FORCE_FAMILY", "IAAT_FORCE_TILE", "IAAT_FORCE_P", "IAAT_FORCE_CTAS", "IAAT_FORCE_ORDER",
+              "IAAT_FORCE_S"):
+        os.environ.pop(k, None)
+    for k, v in kw.items():
+        os.environ["IAAT_FORCE_" + k.upper()] = str(v)
+
+
+@pytest.mark.parametrize("tr", TRANS)
+@pytest.mark.parametrize("dtype", [F32, F64])
+def test_ks_family_parity_and_bitwise_vs_slab(dtype, tr):
+    """The K-streamed TMA plans (forced) against the oracle, on shapes with
+    several tiles, ragged K chunks (K % 32, K % 4 != 0 with 16-byte padded
+    ld), multi-class decompositions and a ragged last unit (batch % P); and
+    fp32 bitwise equal to the slab family (same k-ascending FMA chain per
+    element, same fused epilogue)."""
+    from paper_2208_09822_b200 import iaat
+    try:
+        for (M, N, K) in KS_SHAPES:
+            if tr == "TN" and M * N * K > 32768:
+                continue
+            for P, beta in ((1, 0.5), (3, 0.0)):
+                if P > 1 and M * N > 2048:
+                    continue  # P problems per unit must fit one CTA's warps
+                _force(family=2, p=P)
+                c = Case(dtype, tr[0], tr[1], M, N, K, 301, 21, 1.5, beta, ld_multiple=4)
+                A, B, C = c.views()
+                p = iaat.iaat_plan_describe(0 if dtype == F32 else 1, tr[0], tr[1], M, N, K, c.lda, c.sA, c.ldb,
+                                            c.sB, c.ldc, c.sC, c.batch, beta == 0)
+                assert p["family"].startswith("ks"), (tr, M, N, K, p["family"])
+                c.run()
+                torch.cuda.synchronize()
+                c.check(sample_ids(c.batch, 64, 32))
+                if dtype == F32:
+                    ks = C.clone()
+                    _force()
+                    os_env_default = iaat.iaat_plan_describe(0, tr[0], tr[1], M, N, K, c.lda, c.sA, c.ldb, c.sB,
+                                                             c.ldc, c.sC, c.batch, beta == 0)
+                    c2 = Case(dtype, tr[0], tr[1], M, N, K, 301, 21, 1.5, beta, ld_multiple=4)
+                    _force(family=0)
+                    c2.run()
+                    torch.cuda.synchronize()
+                    assert bits_equal(ks, c2.views()[2]), (tr, M, N, K, os_env_default["family"])
+    finally:
+        _force()
+
+
+def test_ks_not_applicable_falls_back():
+    """Misaligned ld (not a multiple of 16 bytes): no TMA plan exists; a
+    forced KS request falls back to the slab family and stays correct."""
+    from paper_2208_09822_b200 import iaat
+    try:
+        _force(family=2)
+        c = Case(F32, "N", "N", 37, 41, 43, 200, 3, 1.0, 1.0)
+        p = iaat.iaat_plan_describe(0, "N", "N", 37, 41, 43, c.lda, c.sA, c.ldb, c.sB, c.ldc, c.sC, 200, False)
+        assert not p["family"].startswith("ks")
+        c.run()
+        c.check()
+    finally:
+        _force()

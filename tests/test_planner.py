@@ -150,7 +150,13 @@ def test_catalog_register_budget():
         if e["family"] == "fma":
             assert gen.fma_regs(e["dtype"], e["trans"], e["mr"], e["nr"]) <= gen.REG_BUDGET[e["dtype"]]
             assert 1 <= e["mr"] <= 8 and 1 <= e["nr"] <= 8
+        elif e["family"] in ("ks_fma", "ks1_fma"):
+            # K-streamed entries: only those the install-time register check
+            # (tools/ks_regs.py -> gen/ks_unroll.json) accepted
+            assert 1 <= e["mr"] <= 8 and 1 <= e["nr"] <= 8
+            assert gen.ks_unroll(e["dtype"], e["trans"], e["mr"], e["nr"]) > 0
         else:
+            assert e["family"] == "dmma"
             assert e["dtype"] == "f64" and e["mr"] % 8 == 0 and e["nr"] % 8 == 0
     # every (mr, nr) <= 4 x 4 exists for every dtype/trans: any M, N has an exact cover
     for dt in ("f32", "f64"):
