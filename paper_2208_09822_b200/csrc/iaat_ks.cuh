@@ -394,6 +394,148 @@ __device__ __forceinline__ void ks_fma_class_loop(const IaatKsParams &p, const I
     }
 }
 
+// ------------------------------------------------------------------ DMMA class (fp64 warp tile)
+// One warp owns a (8*WM) x (8*WN) block of one problem's C for the whole
+// unit (accumulators in registers across the K-chunks), issued as DMMA.8x8x4
+// (mma.sync.m8n8k4.f64, the only FP64 tensor-core instruction on sm_100a) in
+// the transposed form D' = op(B)^T op(A)^T of iaat_dmma.cuh, so a lane's two
+// accumulators are two consecutive rows of one C column.
+// k mapping inside a chunk: DMMA step s (4 per 16-k chunk) gives position t
+// the k-value 4s + t (the same for both fragments): MN-major operands are
+// then read as 4 consecutive k-rows per half-warp (pitch = 4 mod 16 doubles,
+// conflict-free), K-major ones with at most a 2-way bank conflict.
+// A ragged last chunk reads the copy engine's zero fill past K (0 * 0 adds
+// nothing); no MMA is predicated.
+__device__ __forceinline__ void ks_dmma_8x8x4(double &d0, double &d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// Byte offset (inside a stage region) of element (row r_abs, k) of an fp64
+// operand: K-major swizzled 128-byte rows or MN-major rows of `pitch` doubles.
+template <bool KMAJ>
+__device__ __forceinline__ uint32_t ks_f64_off(int r_abs, int k, int pitch_el, int pk)
+{
+    if (KMAJ) return (((uint32_t)r_abs << 7) | ((uint32_t)((k >> 1) ^ (r_abs & 7)) << 4)) + (uint32_t)(k & 1) * 8u;
+    return (uint32_t)(pk * pitch_el + k * pitch_el + r_abs) * 8u;
+}
+
+template <bool TA, bool TB, int WM, int WN>
+__device__ __forceinline__ void ks_dmma_class_loop(const IaatKsParams &p, const IaatClass &c, unsigned char *smem,
+                                                   uint64_t *full, uint64_t *empty, int warp, int lane)
+{
+    constexpr bool AK = TA, BK = !TB;
+    const int K = p.K, kc = p.kc, nchunks = p.nchunks, P = p.P, S = p.S, M = p.M, N = p.N, ldc = p.ldc;
+    const int stage_bytes = p.stage_bytes, a_bytes = p.a_bytes, dbg = p.debug;
+    const bool beta_zero = p.beta_zero != 0, c_vec = p.c_vec != 0;
+    const int64_t nunits = p.nunits, batch = p.batch;
+    const int g = lane >> 2, t = lane & 3;
+    const int wi = warp - c.warp_begin;
+    const int pl = wi / c.tiles, tt = wi - pl * c.tiles;
+    const int ti = c.colfast ? tt / c.tn : tt % c.tm;
+    const int tj = c.colfast ? tt % c.tn : tt / c.tm;
+    const int row0 = c.row_base + ti * 8 * WM, col0 = c.col_base + tj * 8 * WN;
+    const int pc = min(pl, P - 1);
+    // per-lane offsets of fragment element k = t (step 0 of a chunk); step s
+    // adds 4 k-rows (MN-major) or two 16-byte chunks (K-major, via the XOR)
+    uint32_t oa[WM], ob[WN];
+#pragma unroll
+    for (int mi = 0; mi < WM; ++mi)
+        oa[mi] = AK ? ks_f64_off<true>(pc * M + row0 + 8 * mi + g, t, 0, 0)
+                    : ks_f64_off<false>(row0 + 8 * mi + g, t, p.a_pitch, pc * kc);
+#pragma unroll
+    for (int nj = 0; nj < WN; ++nj)
+        ob[nj] = BK ? ks_f64_off<true>(pc * N + col0 + 8 * nj + g, t, 0, 0)
+                    : ks_f64_off<false>(col0 + 8 * nj + g, t, p.b_pitch, pc * kc);
+    const uint32_t a_step = AK ? 0u : (uint32_t)(4 * p.a_pitch * 8), b_step = BK ? 0u : (uint32_t)(4 * p.b_pitch * 8);
+    const double alpha = p.alpha, beta = p.beta;
+    const int64_t scb = p.sC * 8;
+    const uint32_t ring_off = (uint32_t)(ks_ring(smem) - smem);
+    const bool tile_ok = pl < P;
+
+    int s = 0;
+    uint32_t phase = 0;
+    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int64_t b0 = u * P;
+        const bool active = tile_ok && (b0 + pl) < batch;
+        double acc[WM][WN][2];
+#pragma unroll
+        for (int mi = 0; mi < WM; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < WN; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+        for (int ch = 0; ch < nchunks; ++ch) {
+            mbar_wait(&full[s], phase);
+            if (active && !(dbg & 1)) {
+                const unsigned char *sa = smem + ring_off + (uint32_t)(s * stage_bytes);
+                const unsigned char *sb = sa + a_bytes;
+                const int kv = min(kc, K - ch * kc);
+                const int nsteps = (kv + 3) >> 2;
+#pragma unroll 4
+                for (int st = 0; st < nsteps; ++st) {
+                    double af[WM], bf[WN];
+                    // K-major: k = 4*st + t lives in 16-byte chunk 2*st + t/2 -> XOR (st << 5) on the chunk bits
+#pragma unroll
+                    for (int mi = 0; mi < WM; ++mi)
+                        af[mi] = *reinterpret_cast<const double *>(
+                            sa + (AK ? (oa[mi] ^ ((uint32_t)st << 5)) : oa[mi] + (uint32_t)st * a_step));
+#pragma unroll
+                    for (int nj = 0; nj < WN; ++nj)
+                        bf[nj] = *reinterpret_cast<const double *>(
+                            sb + (BK ? (ob[nj] ^ ((uint32_t)st << 5)) : ob[nj] + (uint32_t)st * b_step));
+#pragma unroll
+                    for (int mi = 0; mi < WM; ++mi)
+#pragma unroll
+                        for (int nj = 0; nj < WN; ++nj) ks_dmma_8x8x4(acc[mi][nj][0], acc[mi][nj][1], bf[nj], af[mi]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == S) {
+                s = 0;
+                phase ^= 1u;
+            }
+        }
+        if (active && !(dbg & 2)) {
+            double *C = reinterpret_cast<double *>(p.C + (b0 + pl) * scb);
+            // per block row: all C_in loads of the row before its stores
+            // (overlapped latencies, bounded registers)
+#pragma unroll
+            for (int mi = 0; mi < WM; ++mi) {
+                double ci[WN][2];
+                if (!beta_zero) {
+#pragma unroll
+                    for (int nj = 0; nj < WN; ++nj) {
+                        const double *cp = C + (row0 + 8 * mi + 2 * t) + (int64_t)(col0 + 8 * nj + g) * ldc;
+                        if (c_vec) {
+                            ldg_vec_cs<double>(cp, ci[nj]);
+                        } else {
+                            ci[nj][0] = ldg_cs(cp);
+                            ci[nj][1] = ldg_cs(cp + 1);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int nj = 0; nj < WN; ++nj) {
+                    double o[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        o[h] = beta_zero ? mul_rn(alpha, acc[mi][nj][h])
+                                         : fma_rn(alpha, acc[mi][nj][h], mul_rn(beta, ci[nj][h]));
+                    double *cp = C + (row0 + 8 * mi + 2 * t) + (int64_t)(col0 + 8 * nj + g) * ldc;
+                    if (c_vec) {
+                        stg_vec_cs<double>(cp, o);
+                    } else {
+                        stg_cs(cp, o[0]);
+                        stg_cs(cp + 1, o[1]);
+                    }
+                }
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ kernel body
 // SINGLE: the plan has one tile class (single-class kernels) -- its fields
 // are then read straight from the constant bank instead of through a

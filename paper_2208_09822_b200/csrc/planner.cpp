@@ -338,6 +338,7 @@ struct Knobs {
 };
 
 Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn);
+bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out);
 
 // ---------------------------------------------------------------- install-time tuning table
 // tuning/b200.tsv next to libiaat.so (written by paper_2208_09822_b200/tune.py on
@@ -415,17 +416,24 @@ Plan make_plan(const PlanRequest &r)
             tuned = true;
         }
     }
+    if (!kn.any() && r.dtype == 1 && r.M % 8 == 0 && r.N % 8 == 0) {
+        // fp64 on tensor cores: the K-streamed DMMA family is the default
+        // wherever its TMA preconditions hold (measured 1.3-2.5x the slab
+        // DMMA kernels on B200, profiles/)
+        Knobs kd;
+        kd.fam = IAAT_FAM_KS_DMMA;
+        Plan pd;
+        if (plan_ks(r, kd, pd)) return pd;
+    }
     Plan p = make_plan_knobs(r, kn);
     if (p.status != 0 && kn.any()) p = make_plan_knobs(r, Knobs());
     else p.tuned = tuned;
     return p;
 }
 
-bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out);
-
 Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn)
 {
-    if (kn.fam == IAAT_FAM_KS_FMA) {
+    if (kn.fam == IAAT_FAM_KS_FMA || kn.fam == IAAT_FAM_KS_DMMA) {
         Plan ksplan;
         if (plan_ks(r, kn, ksplan)) return ksplan;
         ksplan.status = 5;
@@ -759,6 +767,7 @@ namespace {
 struct KsCand {
     bool ok = false;
     int single = 0;
+    int dmma = 0;  // 1: fp64 DMMA warp tiles (one class, one warp tile per warp)
     double total = 1e300, unit = 0;
     int P = 0, S = 0, W = 0, ctas = 1, a_bytes = 0, b_bytes = 0, a_pitch = 0, b_pitch = 0;
     DimSplit ms, ns;
@@ -839,8 +848,10 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
     auto msplits = splits((int)M, 8, vw);
     auto nsplits = splits((int)N, 8, vw);
     KsCand best;
+    const bool want_dmma = kn.fam == IAAT_FAM_KS_DMMA;
     for (const auto &ms : msplits)
         for (const auto &ns : nsplits) {
+            if (want_dmma) break;
             if (kn.mr && (ms.s[0].size != kn.mr || ns.s[0].size != kn.nr)) continue;
             struct Cl {
                 int mr, nr, tm, tn, rb, cb;
@@ -905,6 +916,7 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
                         for (int m = 0; m < 8; ++m) {
                             if (!cl[q].ok[m]) continue;
                             const int w = class_warps(kMaps[m], P, cl[q].tm * cl[q].tn, cl[q].tm, cl[q].tn);
+                            if (W + w > wmax) continue;  // mapping must leave room in the CTA
                             const double k = w * std::max(cl[q].instr[m] / kIssuePerClk, cl[q].wf[m] / kSmemPerClk);
                             if (k < bk * 0.999) {
                                 bk = k;
@@ -974,6 +986,72 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
                 }
             }
         }
+
+    // ---------------- fp64 DMMA warp tiles (one class: (8 wm) x (8 wn) blocks, one per warp)
+    if (want_dmma && r.dtype == 1 && M % 8 == 0 && N % 8 == 0) {
+        // MN-major pitch = 4 (mod 16) doubles: the 4 k-rows a half-warp reads
+        // fall into 4 different 32-byte bank windows
+        auto dpitch = [](int64_t D) { int64_t q = D; while (q % 16 != 4) ++q; return (int)q; };
+        const int da = AK ? kc : dpitch(M), db = BK ? kc : dpitch(N);
+        for (int wm = 1; wm <= 5; ++wm)
+            for (int wn = 1; wn <= 5; ++wn) {
+                if ((M / 8) % wm || (N / 8) % wn) continue;
+                if (kn.mr && (8 * wm != kn.mr || 8 * wn != kn.nr)) continue;
+                if (!catalog_has(1, tidx, IAAT_FAM_KS_DMMA, 8 * wm, 8 * wn)) continue;
+                const int tm = (int)(M / (8 * wm)), tn = (int)(N / (8 * wn)), tiles = tm * tn;
+                for (int ctas = 1; ctas <= 3; ++ctas) {
+                    if (kn.ctas && ctas != kn.ctas) continue;
+                    const int wmax = IAAT_MAX_THREADS / 32 / ctas - 1;
+                    const int smem_cta = (int)std::min<int64_t>(IAAT_SMEM_LIMIT, 228 * 1024 / ctas - 1024);
+                    for (int P = 1; P * tiles <= wmax; ++P) {
+                        if (kn.p && P != kn.p) continue;
+                        if (P > 1 && (int64_t)(P - 1) * r.sm_count * ctas >= r.batch) break;
+                        const int W = P * tiles;
+                        const int a_bytes = (int)round_up((int64_t)P * (AK ? M * 128 : (int64_t)kc * da * 8), 1024);
+                        const int b_bytes = (int)round_up((int64_t)P * (BK ? N * 128 : (int64_t)kc * db * 8), 1024);
+                        const int stage = a_bytes + b_bytes;
+                        int S = std::min(IAAT_KS_MAX_STAGES, (smem_cta - IAAT_KS_BAR_BYTES - 1024) / stage);
+                        if (kn.s > 0) S = std::min(S, kn.s);
+                        if (S < 2) continue;
+                        const double t_hbm = ctas * P * hbm_per_problem / kHbmBytesPerClk;
+                        const double t_dmma = ctas * (double)P * M * N * K / kDfmaPerClk;
+                        const double steps = (double)K / 4;
+                        const double wf = ctas * W * steps * (wm + wn) * 3.0;  // LDS.64: 2 wavefronts, K-major up to 4
+                        const double issue = ctas * W * steps * (wm * wn + (wm + wn) * 2 + 2) / kIssuePerClk;
+                        const double t_lat = kLoadLatency * nchunks / std::max(1, S - 1) / ctas;
+                        const double t_comp = std::max(std::max(t_dmma, wf / kSmemPerClk), issue);
+                        const double t = std::max(std::max(t_hbm, t_comp), t_lat) + 0.15 * std::min(t_hbm, t_comp) + 300.0;
+                        const int64_t nunits = (r.batch + P - 1) / P;
+                        const int64_t slots = (int64_t)r.sm_count * ctas;
+                        const double total = t * (double)((nunits + slots - 1) / slots) + 3000.0;
+                        if (!(total < best.total * 0.995)) continue;
+                        KsCand c;
+                        c.ok = true;
+                        c.dmma = 1;
+                        c.single = 1;
+                        c.total = total;
+                        c.unit = t;
+                        c.P = P;
+                        c.S = S;
+                        c.W = W;
+                        c.ctas = ctas;
+                        c.a_bytes = a_bytes;
+                        c.b_bytes = b_bytes;
+                        c.a_pitch = da;
+                        c.b_pitch = db;
+                        c.ms.s[0] = {8 * wm, tm};
+                        c.ms.n = 1;
+                        c.ns.s[0] = {8 * wn, tn};
+                        c.ns.n = 1;
+                        c.memops = (int64_t)tiles * (8 * wm + 8 * wn) * K + 2 * M * N;
+                        c.ncls = 1;
+                        c.cls[0] = IaatClass{catalog_code(IAAT_FAM_DMMA, 8 * wm, 8 * wn), 0, W, tiles, tm, 0, 8 * wm,
+                                             0, 8 * wn, tn, 0, 0};
+                        best = c;
+                    }
+                }
+            }
+    }
     if (!best.ok) return false;
     Plan &pl = out;
     pl = Plan();
@@ -1021,8 +1099,9 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
     };
     geo(pl.tmA, rowsA, colsA, r.lda, r.sA, AK, best.a_pitch, (int)M);
     geo(pl.tmB, rowsB, colsB, r.ldb, r.sB, BK, best.b_pitch, (int)N);
-    pl.family = IAAT_FAM_KS_FMA;
+    pl.family = best.dmma ? IAAT_FAM_KS_DMMA : IAAT_FAM_KS_FMA;
     pl.single = best.single;
+    pl.ksd = best.dmma;
     pl.vec = 1;
     pl.ctas = best.ctas;
     pl.grid = (int)std::min<int64_t>(k.nunits, (int64_t)r.sm_count * best.ctas);
@@ -1064,7 +1143,7 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
         const IaatKsParams &q = p.ksp;
         add("\"family\": \"%s\", \"vec\": %d, \"P\": %d, \"S\": %d, \"compute_warps\": %d, "
             "\"ctas_per_sm\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, \"ngroups\": %lld, ",
-            p.single ? "ks1_fma" : "ks_fma", p.vec, q.P, q.S, q.n_compute_warps, p.ctas, p.grid, p.block, p.smem,
+            p.ksd ? "ks_dmma" : p.single ? "ks1_fma" : "ks_fma", p.vec, q.P, q.S, q.n_compute_warps, p.ctas, p.grid, p.block, p.smem,
             (long long)q.nunits);
         add("\"kc\": %d, \"nchunks\": %d, \"a_bytes\": %d, \"b_bytes\": %d, \"a_pitch\": %d, \"b_pitch\": %d, "
             "\"a_swizzle128\": %d, \"b_swizzle128\": %d, \"c_vec\": %d, ",

@@ -42,6 +42,7 @@ struct Plan {
     IaatKParams kp{};      // pointers / alpha / beta filled at call time
     int ks = 0;            // 1: K-streamed family (ksp + tmA/tmB are the plan)
     int single = 0;        // K-streamed: 1 = a single-class kernel (tile ksp.cls[0].mr x nr)
+    int ksd = 0;           // K-streamed: 1 = fp64 DMMA warp-tile kernel (iaat_ksd_*)
     IaatKsParams ksp{};
     TmaGeo tmA{}, tmB{};
     int grid = 0, block = 0, smem = 0;

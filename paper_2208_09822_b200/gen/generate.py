@@ -104,6 +104,10 @@ def catalog():
                              "code": fma_code(mr, nr)})
         if dt == "f64":
             for tr in TRANS:
+                for wm, wn in KSD_TILES:
+                    ents.append({"family": "ks_dmma", "dtype": dt, "trans": tr, "mr": 8 * wm, "nr": 8 * wn,
+                                 "code": dmma_code(wm, wn)})
+            for tr in TRANS:
                 for wm, wn in dmma_tiles(tr):
                     ents.append({"family": "dmma", "dtype": dt, "trans": tr, "mr": 8 * wm,
                                  "nr": 8 * wn, "code": dmma_code(wm, wn)})
@@ -195,6 +199,49 @@ KS1_TILES = {
 
 
 _KS_UNROLL = None
+
+
+# fp64 DMMA warp tiles of the K-streamed family: (wm, wn) blocks of 8 x 8,
+# accumulators 4*wm*wn registers <= 64
+KSD_TILES = [(wm, wn) for wm in range(1, 6) for wn in range(1, 6) if wm * wn <= 16]
+
+
+def ksd_kernel_name(tr, wm, wn):
+    return "iaat_ksd_f64_%s_%dx%d" % (tr, wm, wn)
+
+
+def gen_ksd_file(tr):
+    """Single-class K-streamed DMMA kernels (fp64) of one transposition."""
+    ta = "true" if tr[0] == "T" else "false"
+    tb = "true" if tr[1] == "T" else "false"
+    parts = []
+    for wm, wn in KSD_TILES:
+        name = ksd_kernel_name(tr, wm, wn)
+        parts.append("""
+struct Dispatch_%(name)s {
+    static __device__ __forceinline__ void run(const IaatKsParams &p, const IaatClass &c,
+                                               unsigned char *smem, uint64_t *full,
+                                               uint64_t *empty, int warp, int lane)
+    {
+        ks_dmma_class_loop<%(ta)s, %(tb)s, %(wm)d, %(wn)d>(p, c, smem, full, empty, warp, lane);
+    }
+};
+
+__global__ void __launch_bounds__(IAAT_MAX_THREADS, 1)
+%(name)s(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+         const __grid_constant__ IaatKsParams p)
+{
+    ks_kernel_body<double, %(ta)s, %(tb)s, Dispatch_%(name)s, true>(&tmA, &tmB, p);
+}
+%(launch)s""" % {"name": name, "ta": ta, "tb": tb, "wm": wm, "wn": wn, "launch": KS_LAUNCH % {"name": name}})
+    return """// GENERATED by gen/generate.py -- do not edit.  K-streamed DMMA (fp64 tensor-core)
+// kernels, trans=%s (install-time stage, PAPER.md:74-105).
+#include "../iaat_ks.cuh"
+
+namespace iaat {
+%s
+}  // namespace iaat
+""" % (tr, "".join(parts))
 
 
 def ks_unroll(dt, tr, mr, nr):
@@ -327,7 +374,7 @@ def gen_table():
         for tr in TRANS:
             tb.append("{&launch_%s, &launch_%s}" % (kernel_name(dt, tr, 0), kernel_name(dt, tr, 1)))
         body.append("    {" + ", ".join(tb) + "}")
-    ks_decl, ks_body, ks1 = [], [], []
+    ks_decl, ks_body, ks1, ksd = [], [], [], []
     for dt in DTYPES:
         for tr in TRANS:
             ks_decl.append("cudaError_t launch_%s(const CUtensorMap &, const CUtensorMap &, const IaatKsParams &, "
@@ -337,6 +384,11 @@ def gen_table():
                                "int, int, int, cudaStream_t);" % ks1_kernel_name(dt, tr, mr, nr))
                 ks1.append("    {%d, %d, %d, %d, &launch_%s}," % (list(DTYPES).index(dt), TRANS.index(tr), mr, nr,
                                                                   ks1_kernel_name(dt, tr, mr, nr)))
+            if dt == "f64":
+                for wm, wn in KSD_TILES:
+                    ks_decl.append("cudaError_t launch_%s(const CUtensorMap &, const CUtensorMap &, "
+                                   "const IaatKsParams &, int, int, int, cudaStream_t);" % ksd_kernel_name(tr, wm, wn))
+                    ksd.append("    {%d, %d, %d, &launch_%s}," % (TRANS.index(tr), wm, wn, ksd_kernel_name(tr, wm, wn)))
         ks_body.append("    {" + ", ".join("&launch_%s" % ks_kernel_name(dt, tr) for tr in TRANS) + "}")
     return ("// GENERATED by gen/generate.py -- launch table [dtype][trans NN,NT,TN,TT][vec]\n"
             "namespace iaat {\n" + "\n".join(decl) +
@@ -348,6 +400,8 @@ def gen_table():
             "static const KsLaunchFn kLaunchKs[2][4] = {\n" + ",\n".join(ks_body) + "\n};\n"
             "struct Ks1Entry { int dtype, trans, mr, nr; KsLaunchFn fn; };\n"
             "static const Ks1Entry kLaunchKs1[] = {\n" + "\n".join(ks1) + "\n};\n"
+            "struct KsdEntry { int trans, wm, wn; KsLaunchFn fn; };\n"
+            "static const KsdEntry kLaunchKsd[] = {\n" + "\n".join(ksd) + "\n};\n"
             "}  // namespace iaat\n")
 
 
@@ -399,6 +453,10 @@ def main(argv=None):
             p = os.path.join(args.out, "ks1_%s_%s.cu" % (dt, tr))
             write_if_changed(p, gen_ks1_file(dt, tr))
             files.append(p)
+            if dt == "f64":
+                p = os.path.join(args.out, "ksd_f64_%s.cu" % tr)
+                write_if_changed(p, gen_ksd_file(tr))
+                files.append(p)
     return files
 
 

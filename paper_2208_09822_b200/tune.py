@@ -158,7 +158,7 @@ def tune_shape(sh, log):
             p = b.plan()
             if p["status"] != 0:
                 return None
-            if kw.get("family") == 2 and not p["family"].startswith("ks"):
+            if kw.get("family") in (2, 3) and not p["family"].startswith("ks"):
                 return None  # K-streamed plan not applicable: the planner fell back
             us = b.time_us()
         except Exception:
@@ -178,6 +178,13 @@ def tune_shape(sh, log):
         for (wm, wn) in ((1, 1), (1, 2), (2, 1), (2, 2)):
             for P in Ps:
                 trial(tile="%dx%d" % (8 * wm, 8 * wn), p=P, family=1)
+    if dtype == "f64" and M % 8 == 0 and N % 8 == 0:  # K-streamed DMMA warp tiles
+        for a in range(1, 6):
+            for bb in range(1, 6):
+                if a * bb <= 16 and 8 * a <= M and 8 * bb <= N:
+                    for P in (1, 2, 3, 4):
+                        for ctas in (1, 2, 3):
+                            trial(family=3, tile="%dx%d" % (8 * a, 8 * bb), p=P, ctas=ctas)
     if max(M, N, K) >= 20:  # K-streamed TMA family (csrc/iaat_ks.cuh)
         ks_tiles = [t for t in ("4x8", "8x4", "4x4", "6x8", "8x6", "5x8", "8x5", "4x6", "6x4", "2x8", "8x2")
                     if int(t.split("x")[0]) <= M and int(t.split("x")[1]) <= N]
@@ -192,7 +199,7 @@ def tune_shape(sh, log):
             for P in sorted({max(1, int(kb * 1024) // per_ab) for kb in (24, 48, 96)}):
                 trial(tile="%dx%d" % (mr, nr), p=P, csmem=0)
     results.sort(key=lambda x: x[0])
-    top = [r for r in results if r[1].get("family") != 2][:4]
+    top = [r for r in results if r[1].get("family") not in (2, 3)][:4]
     for us, kw, p in top:
         for order in (0, 1, 3, 5, 9, 17):
             for ctas in (1, 2, 3, 4):

@@ -412,3 +412,33 @@ def test_ks_not_applicable_falls_back():
         c.check()
     finally:
         _force()
+
+
+@pytest.mark.parametrize("tr", TRANS)
+def test_ks_dmma_fp64_parity(tr):
+    """fp64 K-streamed DMMA warp tiles (forced family 3) against the oracle:
+    every warp-tile size that divides the shape, ragged K chunks (K % 16,
+    K % 4 != 0 -> the copy engine's zero fill feeds the last DMMA step),
+    a ragged last unit, beta = 0 and beta != 0."""
+    from paper_2208_09822_b200 import iaat
+    shapes = [(64, 64, 64), (80, 80, 80), (48, 32, 40), (16, 24, 37), (8, 8, 8)]
+    try:
+        for (M, N, K) in shapes:
+            if tr == "TN" and M * N * K > 32768:
+                continue
+            for wm in (1, 2, 4, 5):
+                for wn in (1, 2, 3, 5):
+                    if (M // 8) % wm or (N // 8) % wn:
+                        continue
+                    for beta, P in ((0.0, 1), (0.5, 2)):
+                        _force(family=3, tile="%dx%d" % (8 * wm, 8 * wn), p=P)
+                        c = Case(F64, tr[0], tr[1], M, N, K, 203, 31, -1.25, beta, ld_multiple=2)
+                        p = iaat.iaat_plan_describe(1, tr[0], tr[1], M, N, K, c.lda, c.sA, c.ldb, c.sB, c.ldc, c.sC,
+                                                    c.batch, beta == 0)
+                        if p["family"] != "ks_dmma":
+                            continue  # (P x tiles) does not fit one CTA
+                        c.run()
+                        torch.cuda.synchronize()
+                        c.check(sample_ids(c.batch, 48, 24))
+    finally:
+        _force()

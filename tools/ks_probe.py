@@ -46,15 +46,20 @@ def main():
         base = b.time_us()
         print("%s %s n=%d batch=%d: default plan %.1f us  plan=%s" % (dtype, tr, n, b.batch, base,
                                                                     b.plan()["family"]), flush=True)
-        tiles = ["4x8", "8x4", "4x4", "6x8", "8x6", "5x8", "8x5", "4x6", "6x4"]
-        for tile, order, P, ctas in itertools.product(tiles, (0, 1, 5, 9), (1, 2, 3), (1, 2, 3)):
-            kw = dict(family=2, tile=tile, order=order, p=P, ctas=ctas)
+        if dtype == "f64":
+            tiles = ["%dx%d" % (8 * a, 8 * b) for a in range(1, 6) for b in range(1, 6) if a * b <= 16]
+            grid = [dict(family=3, tile=t, p=P, ctas=c) for t in tiles for P in (1, 2, 3, 4) for c in (1, 2, 3)]
+        else:
+            tiles = ["4x8", "8x4", "4x4", "6x8", "8x6", "5x8", "8x5", "4x6", "6x4"]
+            grid = [dict(family=2, tile=t, order=o, p=P, ctas=c)
+                    for t, o, P, c in itertools.product(tiles, (0, 1, 5, 9), (1, 2, 3), (1, 2, 3))]
+        for kw in grid:
             set_knobs(**kw)
             try:
                 p = b.plan()
                 if p["status"] != 0 or not p["family"].startswith("ks"):
                     continue
-                key = (tile, p["classes"][0]["bm"], p["classes"][0]["colfast"], p["P"], p["ctas_per_sm"])
+                key = (kw["tile"], p["classes"][0]["bm"], p["classes"][0]["colfast"], p["P"], p["ctas_per_sm"])
                 if any(r[2] == key for r in res):
                     continue
                 us = b.time_us()
