@@ -172,6 +172,124 @@ __device__ __forceinline__ double fma_rn(double a, double b, double c) { return 
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 
+// ------------------------------------------------------------------ register tile
+// The C_c register block of one lane (Cregs) with the
+// rank-1 update acc(i,j) += a(i) * b(j).  fp32 tiles are held as 64-bit
+// register pairs and updated with FFMA2 (fma.rn.f32x2, sm_100a: two
+// independent IEEE fp32 FMAs per instruction -- bitwise the same as two
+// FFMAs, half the issue slots); the scalar operand is a broadcast that ptxas
+// folds into the instruction (Rn.F32).  PAIR: 1 = pairs along i (the a
+// fragment arrives as consecutive registers from a 16-byte load), 2 = pairs
+// along j, 0 = scalar FMAs (fp64, or no even dimension).
+__device__ __forceinline__ unsigned long long pack_f32x2(float lo, float hi)
+{
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+
+__device__ __forceinline__ void unpack_f32x2(unsigned long long v, float &lo, float &hi)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+
+__device__ __forceinline__ void ffma2(unsigned long long &c, unsigned long long a, unsigned long long b)
+{
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(a), "l"(b));
+}
+
+template <typename T, int MR, int NR, int PAIR>
+struct RegTile {
+    T v[MR][NR];
+    __device__ __forceinline__ void zero()
+    {
+#pragma unroll
+        for (int i = 0; i < MR; ++i)
+#pragma unroll
+            for (int j = 0; j < NR; ++j) v[i][j] = (T)0;
+    }
+    template <typename AF, typename BF>
+    __device__ __forceinline__ void rank1(const AF &a, const BF &b)
+    {
+#pragma unroll
+        for (int j = 0; j < NR; ++j)
+#pragma unroll
+            for (int i = 0; i < MR; ++i) v[i][j] = fma_rn(a(i), b(j), v[i][j]);
+    }
+    __device__ __forceinline__ void get(T (&o)[MR][NR]) const
+    {
+#pragma unroll
+        for (int i = 0; i < MR; ++i)
+#pragma unroll
+            for (int j = 0; j < NR; ++j) o[i][j] = v[i][j];
+    }
+};
+
+template <int MR, int NR>
+struct RegTile<float, MR, NR, 1> {  // pairs (i, i+1)
+    unsigned long long v[MR / 2][NR];
+    __device__ __forceinline__ void zero()
+    {
+#pragma unroll
+        for (int i = 0; i < MR / 2; ++i)
+#pragma unroll
+            for (int j = 0; j < NR; ++j) v[i][j] = 0ull;
+    }
+    template <typename AF, typename BF>
+    __device__ __forceinline__ void rank1(const AF &a, const BF &b)
+    {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+            const unsigned long long bb = pack_f32x2(b(j), b(j));
+#pragma unroll
+            for (int i = 0; i < MR / 2; ++i) ffma2(v[i][j], pack_f32x2(a(2 * i), a(2 * i + 1)), bb);
+        }
+    }
+    __device__ __forceinline__ void get(float (&o)[MR][NR]) const
+    {
+#pragma unroll
+        for (int i = 0; i < MR / 2; ++i)
+#pragma unroll
+            for (int j = 0; j < NR; ++j) unpack_f32x2(v[i][j], o[2 * i][j], o[2 * i + 1][j]);
+    }
+};
+
+template <int MR, int NR>
+struct RegTile<float, MR, NR, 2> {  // pairs (j, j+1)
+    unsigned long long v[MR][NR / 2];
+    __device__ __forceinline__ void zero()
+    {
+#pragma unroll
+        for (int i = 0; i < MR; ++i)
+#pragma unroll
+            for (int j = 0; j < NR / 2; ++j) v[i][j] = 0ull;
+    }
+    template <typename AF, typename BF>
+    __device__ __forceinline__ void rank1(const AF &a, const BF &b)
+    {
+#pragma unroll
+        for (int j = 0; j < NR / 2; ++j) {
+            const unsigned long long bb = pack_f32x2(b(2 * j), b(2 * j + 1));
+#pragma unroll
+            for (int i = 0; i < MR; ++i) ffma2(v[i][j], pack_f32x2(a(i), a(i)), bb);
+        }
+    }
+    __device__ __forceinline__ void get(float (&o)[MR][NR]) const
+    {
+#pragma unroll
+        for (int i = 0; i < MR; ++i)
+#pragma unroll
+            for (int j = 0; j < NR / 2; ++j) unpack_f32x2(v[i][j], o[i][2 * j], o[i][2 * j + 1]);
+    }
+};
+
+// Pairing choice: along the dimension whose fragment arrives as consecutive
+// registers (contiguous in smem); fp64 and odd tiles use scalar FMAs.
+template <typename T, bool A_CONTIG, bool B_CONTIG, int MR, int NR>
+struct PairOf {
+    static constexpr int value = sizeof(T) != 4 ? 0 : (A_CONTIG && MR % 2 == 0) ? 1 : (B_CONTIG && NR % 2 == 0) ? 2 : 0;
+};
+
 // ------------------------------------------------------------------ smem layout
 struct StageView {
     unsigned char *a;  // this stage's A region
@@ -359,8 +477,8 @@ __device__ __forceinline__ void load_one(T (&f)[R], const T *X, int ld, int k, i
 }
 
 // acc(i,j) += sum_k opA(row0+i, k) * opB(k, col0+j), k ascending, one FMA each.
-template <typename T, bool TA, bool TB, int MR, int NR, bool VEC, int UNR>
-__device__ __forceinline__ void fma_tile(T (&acc)[MR][NR], const T *__restrict__ sA,
+template <typename T, bool TA, bool TB, int MR, int NR, bool VEC, int UNR, typename ACC>
+__device__ __forceinline__ void fma_tile(ACC &acc, const T *__restrict__ sA,
                                          const T *__restrict__ sB, int lda, int ldb, int K,
                                          int row0, int col0)
 {
@@ -376,21 +494,14 @@ __device__ __forceinline__ void fma_tile(T (&acc)[MR][NR], const T *__restrict__
         load_frag<T, TA, MR, VEC>(a, sA, lda, k, row0);
         load_frag<T, !TB, NR, VEC>(b, sB, ldb, k, col0);
 #pragma unroll
-        for (int kk = 0; kk < KU; ++kk)
-#pragma unroll
-            for (int j = 0; j < NR; ++j)
-#pragma unroll
-                for (int i = 0; i < MR; ++i) acc[i][j] = fma_rn(a[kk][i], b[kk][j], acc[i][j]);
+        for (int kk = 0; kk < KU; ++kk) acc.rank1([&](int i) { return a[kk][i]; }, [&](int j) { return b[kk][j]; });
     }
 #pragma unroll 1
     for (; k < K; ++k) {
         T a[MR], b[NR];
         load_one<T, TA, MR>(a, sA, lda, k, row0);
         load_one<T, !TB, NR>(b, sB, ldb, k, col0);
-#pragma unroll
-        for (int j = 0; j < NR; ++j)
-#pragma unroll
-            for (int i = 0; i < MR; ++i) acc[i][j] = fma_rn(a[i], b[j], acc[i][j]);
+        acc.rank1([&](int i) { return a[i]; }, [&](int j) { return b[j]; });
     }
 }
 
@@ -516,11 +627,9 @@ __device__ __forceinline__ void fma_class_loop(const IaatKParams &p, const IaatC
         const int64_t b0 = g * p.P;
         const int np = (int)min((int64_t)p.P, p.batch - b0);
         const bool active = tile_ok && pl < np;
-        T acc[MR][NR];
-#pragma unroll
-        for (int i = 0; i < MR; ++i)
-#pragma unroll
-            for (int j = 0; j < NR; ++j) acc[i][j] = (T)0;
+        // A tile-contiguous iff !TA, B tile-contiguous iff TB (see load_frag)
+        RegTile<T, MR, NR, PairOf<T, !TA, TB, MR, NR>::value> acc;
+        acc.zero();
         mbar_wait(&full[s], (it / p.S) & 1);
         if (active) {
             StageView sv = stage_view(p, smem, s);
@@ -548,7 +657,9 @@ __device__ __forceinline__ void fma_class_loop(const IaatKParams &p, const IaatC
                 Cin = reinterpret_cast<const T *>(
                     sv.c + smem_offset(p.modeC, c_first, c_prob, scb, p.slotC, pl));
             }
-            epilogue<T, MR, NR, VEC>(acc, C, Cin, p.ldc, row0, col0, alpha, beta, p.beta_zero != 0);
+            T accv[MR][NR];
+            acc.get(accv);
+            epilogue<T, MR, NR, VEC>(accv, C, Cin, p.ldc, row0, col0, alpha, beta, p.beta_zero != 0);
         }
         if (p.c_in_smem) {
             __syncwarp();

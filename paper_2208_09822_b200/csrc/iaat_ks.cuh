@@ -189,8 +189,8 @@ __device__ __forceinline__ void ks_frag_load(KsFrag<T, AK, BK, MR, NR> &f, const
 }
 
 // acc(i,j) += sum over the KU k-steps of the block, k ascending, one FMA each.
-template <typename T, bool AK, bool BK, bool UA, bool UB, int MR, int NR>
-__device__ __forceinline__ void ks_frag_fma(T (&acc)[MR][NR], const KsFrag<T, AK, BK, MR, NR> &f,
+template <typename T, bool AK, bool BK, bool UA, bool UB, int MR, int NR, typename ACC>
+__device__ __forceinline__ void ks_frag_fma(ACC &acc, const KsFrag<T, AK, BK, MR, NR> &f,
                                             const unsigned char *smem, const KsOpnd<AK, UA, MR> &oa,
                                             const KsOpnd<BK, UB, NR> &ob, uint32_t a_mn, uint32_t b_mn, int kb)
 {
@@ -205,14 +205,9 @@ __device__ __forceinline__ void ks_frag_fma(T (&acc)[MR][NR], const KsFrag<T, AK
             if (!BK) ks_load_mn<T, NR>(reinterpret_cast<T (&)[NR]>(mb[(kk + 1) & 1]), smem,
                                        b0 + (uint32_t)(kk + 1) * ob.pitch);
         }
-#pragma unroll
-        for (int j = 0; j < NR; ++j)
-#pragma unroll
-            for (int i = 0; i < MR; ++i) {
-                const T av = AK ? f.ka[AK ? kk : 0][i] : (kk == 0 ? f.ma[AK ? 0 : i] : ma[kk & 1][AK ? 0 : i]);
-                const T bv = BK ? f.kb[BK ? kk : 0][j] : (kk == 0 ? f.mb[BK ? 0 : j] : mb[kk & 1][BK ? 0 : j]);
-                acc[i][j] = fma_rn(av, bv, acc[i][j]);
-            }
+        acc.rank1(
+            [&](int i) { return AK ? f.ka[AK ? kk : 0][i] : (kk == 0 ? f.ma[AK ? 0 : i] : ma[kk & 1][AK ? 0 : i]); },
+            [&](int j) { return BK ? f.kb[BK ? kk : 0][j] : (kk == 0 ? f.mb[BK ? 0 : j] : mb[kk & 1][BK ? 0 : j]); });
     }
 }
 
@@ -220,8 +215,8 @@ __device__ __forceinline__ void ks_frag_fma(T (&acc)[MR][NR], const KsFrag<T, AK
 // of the stage's A / B regions from the smem base; ra / rb: the lane's
 // swizzled row / column bases inside a region (K-major operands), a_mn /
 // b_mn: the lane's first element inside a region (MN-major operands).
-template <typename T, bool AK, bool BK, bool UA, bool UB, int MR, int NR, int UNR, int NA, int NB>
-__device__ __forceinline__ void ks_chunk(T (&acc)[MR][NR], const unsigned char *smem, uint32_t sa, uint32_t sb,
+template <typename T, bool AK, bool BK, bool UA, bool UB, int MR, int NR, int UNR, int NA, int NB, typename ACC>
+__device__ __forceinline__ void ks_chunk(ACC &acc, const unsigned char *smem, uint32_t sa, uint32_t sb,
                                          const uint32_t (&ra)[NA], const uint32_t (&rb)[NB], uint32_t a_mn,
                                          uint32_t b_mn, uint32_t a_pitch, uint32_t b_pitch, uint32_t a_rs,
                                          uint32_t b_rs, int kv)
@@ -276,10 +271,7 @@ __device__ __forceinline__ void ks_chunk(T (&acc)[MR][NR], const unsigned char *
         for (int j = 0; j < NR; ++j)
             b[j] = BK ? *reinterpret_cast<const T *>(smem + ((UB ? (ob.base[0] ^ q) + j * b_rs : (ob.base[BK && !UB ? j : 0] ^ q)) + w))
                       : *reinterpret_cast<const T *>(smem + bm + (uint32_t)kb * b_pitch + j * sizeof(T));
-#pragma unroll
-        for (int j = 0; j < NR; ++j)
-#pragma unroll
-            for (int i = 0; i < MR; ++i) acc[i][j] = fma_rn(a[i], b[j], acc[i][j]);
+        acc.rank1([&](int i) { return a[i]; }, [&](int j) { return b[j]; });
     }
 }
 
@@ -350,11 +342,8 @@ __device__ __forceinline__ void ks_fma_class_loop(const IaatKsParams &p, const I
     for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int64_t b0 = u * P;
         const bool active = tile_ok && (b0 + pl) < batch && pl < P;
-        T acc[MR][NR];
-#pragma unroll
-        for (int i = 0; i < MR; ++i)
-#pragma unroll
-            for (int j = 0; j < NR; ++j) acc[i][j] = (T)0;
+        RegTile<T, MR, NR, PairOf<T, !AK, !BK, MR, NR>::value> acc;
+        acc.zero();
         for (int ch = 0; ch < nchunks; ++ch) {
             if (!(dbg & 4)) mbar_wait(&full[s], phase);
             if (active && !(dbg & 1)) {
@@ -384,11 +373,13 @@ __device__ __forceinline__ void ks_fma_class_loop(const IaatKsParams &p, const I
         if (active && !(dbg & 2)) {
             // fused epilogue: C = alpha*acc + beta*C_in (C_in never read when beta == 0)
             T *C = reinterpret_cast<T *>(Cbase + (b0 + pl) * scb);
+            T accv[MR][NR];
+            acc.get(accv);
             if (!AK && c_vec)
-                epilogue_tile<T, MR, NR, true, true>(acc, C, C, ldc, row0, 1, col0, BK ? tn : 1, alpha, beta,
+                epilogue_tile<T, MR, NR, true, true>(accv, C, C, ldc, row0, 1, col0, BK ? tn : 1, alpha, beta,
                                                      beta_zero);
             else
-                epilogue_tile<T, MR, NR, false, true>(acc, C, C, ldc, row0, AK ? tm : 1, col0, BK ? tn : 1, alpha,
+                epilogue_tile<T, MR, NR, false, true>(accv, C, C, ldc, row0, AK ? tm : 1, col0, BK ? tn : 1, alpha,
                                                       beta, beta_zero);
         }
     }

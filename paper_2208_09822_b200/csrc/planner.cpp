@@ -899,9 +899,12 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
                 rb += ms.s[a].size * ms.s[a].count;
             }
             if (!avail) continue;
-            for (int ctas = 1; ctas <= 3; ++ctas) {
+            for (int ctas = 1; ctas <= 4; ++ctas) {
                 if (kn.ctas && ctas != kn.ctas) continue;
-                const int wmax = IAAT_MAX_THREADS / 32 / ctas - 1;
+                // 128 registers per thread -> at most 16 resident warps per SM
+                // (4 per SM sub-partition), producers included
+                const int wmax = std::min(IAAT_MAX_THREADS / 32, 16 / ctas) - 1;
+                if (wmax < 1) continue;
                 const int smem_cta = (int)std::min<int64_t>(IAAT_SMEM_LIMIT, 228 * 1024 / ctas - 1024);
                 for (int P = 1; P <= 64; ++P) {
                     if (kn.p && P != kn.p) continue;

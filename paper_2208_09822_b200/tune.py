@@ -190,8 +190,8 @@ def tune_shape(sh, log):
                     if int(t.split("x")[0]) <= M and int(t.split("x")[1]) <= N]
         for tile in ks_tiles:
             for order in (0, 1, 5, 9):
-                for P in (1, 2, 3):
-                    for ctas in (1, 2, 3):
+                for P in (1, 2, 3, 4):
+                    for ctas in (1, 2, 3, 4):
                         trial(family=2, tile=tile, order=order, p=P, ctas=ctas)
     if beta != 0:  # C_in from global (L2-prefetched) instead of staged: frees smem
         per_ab = (M * K + K * N) * elt

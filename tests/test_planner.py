@@ -67,7 +67,14 @@ def check_plan(p, dt, tr, M, N):
     assert wprev == p["compute_warps"] <= 15
     assert p["block"] == 32 * (p["compute_warps"] + 1)
     assert p["smem"] <= 227 * 1024
-    assert 1 <= p["S"] <= 6
+    if p["family"].startswith("ks"):
+        # K-streamed: S-stage ring of K-chunks, 1024-byte aligned stages
+        assert 2 <= p["S"] <= 12
+        assert p["a_bytes"] % 1024 == 0 and p["b_bytes"] % 1024 == 0
+        assert p["kc"] * (4 if dt == 0 else 8) == 128
+        assert p["nchunks"] * p["kc"] >= p["K"] > (p["nchunks"] - 1) * p["kc"]
+    else:
+        assert 1 <= p["S"] <= 6
     assert p["grid"] <= 148 * p["ctas_per_sm"]
 
 
@@ -156,7 +163,7 @@ def test_catalog_register_budget():
             assert 1 <= e["mr"] <= 8 and 1 <= e["nr"] <= 8
             assert gen.ks_unroll(e["dtype"], e["trans"], e["mr"], e["nr"]) > 0
         else:
-            assert e["family"] == "dmma"
+            assert e["family"] in ("dmma", "ks_dmma")
             assert e["dtype"] == "f64" and e["mr"] % 8 == 0 and e["nr"] % 8 == 0
     # every (mr, nr) <= 4 x 4 exists for every dtype/trans: any M, N has an exact cover
     for dt in ("f32", "f64"):

@@ -52,14 +52,14 @@ def main():
         else:
             tiles = ["4x8", "8x4", "4x4", "6x8", "8x6", "5x8", "8x5", "4x6", "6x4"]
             grid = [dict(family=2, tile=t, order=o, p=P, ctas=c)
-                    for t, o, P, c in itertools.product(tiles, (0, 1, 5, 9), (1, 2, 3), (1, 2, 3))]
+                    for t, o, P, c in itertools.product(tiles, (0, 1, 5, 9), (1, 2, 3, 4), (1, 2, 3, 4))]
         for kw in grid:
             set_knobs(**kw)
             try:
                 p = b.plan()
                 if p["status"] != 0 or not p["family"].startswith("ks"):
                     continue
-                key = (kw["tile"], p["classes"][0]["bm"], p["classes"][0]["colfast"], p["P"], p["ctas_per_sm"])
+                key = (kw["family"], kw["tile"], p["classes"][0]["bm"], p["classes"][0]["colfast"], p["P"], p["ctas_per_sm"])
                 if any(r[2] == key for r in res):
                     continue
                 us = b.time_us()

@@ -32,14 +32,14 @@ struct D {
         ks_fma_class_loop<%s, %s, %s, %d, %d, %d>(p, c, smem, full, empty, warp, lane);
     }
 };
-__global__ void __launch_bounds__(IAAT_MAX_THREADS, 1)
+__global__ void __launch_bounds__(%s, 1)
 kcase(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
       const __grid_constant__ IaatKsParams p)
 {
     ks_kernel_body<%s, %s, %s, D, true>(&tmA, &tmB, p);
 }
 }
-""" % (T, ta, tb, mr, nr, unr, T, ta, tb)
+""" % (T, ta, tb, mr, nr, unr, "IAAT_MAX_THREADS", T, ta, tb)
     fn = os.path.join(out, "c_%s_%s_%d_%d_%d.cu" % (dt, tr, mr, nr, unr))
     open(fn, "w").write(src)
     r = subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xptxas", "-v",

@@ -1,0 +1,1 @@
+timeout 600 python tools/ks_probe.py f32 NN 80 f32 TT 80 f32 NN 64 f32 NT 64 f32 TT 64 > gpurun_out/ks39.log 2>&1; echo probe=$?
