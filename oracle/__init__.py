@@ -52,6 +52,12 @@ def _load():
             vp, i64, i64, vp, i64, i64, dbl, vp, i64, i64, i64, vp, vp,
             ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
         lib.iaat_ref_gemm.restype = ctypes.c_int
+        dp = ctypes.POINTER(ctypes.c_double)
+        lib.iaat_ref_cgemm.argtypes = [
+            ctypes.c_int, ctypes.c_char, ctypes.c_char, i64, i64, i64, dp,
+            vp, i64, i64, vp, i64, i64, dp, vp, i64, i64, i64, vp, vp,
+            ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        lib.iaat_ref_cgemm.restype = ctypes.c_int
         lib.iaat_ref_is_small.argtypes = [ctypes.c_char, ctypes.c_char, i64, i64, i64]
         lib.iaat_ref_is_small.restype = ctypes.c_int
         _lib = lib
@@ -89,6 +95,48 @@ def ref_gemm(transA, transB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
     if rc != 0:
         raise ValueError("iaat_ref_gemm rejected its arguments")
     return ref, den, used.value
+
+
+def ref_cgemm(transA, transB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
+              beta, C, ldc, strideC, batch, nthreads: int = 0, want_den=True):
+    """Complex reference (CGEMM / ZGEMM): A, B, C flat complex64 / complex128
+    numpy arrays (interleaved re, im), ld's and strides in complex elements,
+    alpha / beta Python complex.  Returns (ref, den, threads): ref complex128
+    of shape (batch, N, M), den float64 (batch, N, M) with the 1-norm bound
+    of oracle/ref_gemm.c."""
+    A = np.ascontiguousarray(A)
+    B = np.ascontiguousarray(B)
+    dtype = {np.dtype(np.complex64): 2, np.dtype(np.complex128): 3}[A.dtype]
+    assert B.dtype == A.dtype
+    alpha, beta = complex(alpha), complex(beta)
+    if C is not None:
+        C = np.ascontiguousarray(C)
+        assert C.dtype == A.dtype
+    ref = np.empty((batch, N, M), dtype=np.complex128)
+    den = np.empty((batch, N, M), dtype=np.float64) if want_den else None
+    al = (ctypes.c_double * 2)(alpha.real, alpha.imag)
+    be = (ctypes.c_double * 2)(beta.real, beta.imag)
+    used = ctypes.c_int(0)
+    rc = _load().iaat_ref_cgemm(
+        dtype, transA.encode(), transB.encode(), M, N, K, al,
+        _ptr(A), lda, strideA, _ptr(B), ldb, strideB, be,
+        _ptr(C) if (C is not None and beta != 0) else None, ldc, strideC, batch,
+        _ptr(ref), _ptr(den), int(nthreads), ctypes.byref(used))
+    if rc != 0:
+        raise ValueError("iaat_ref_cgemm rejected its arguments")
+    return ref, den, used.value
+
+
+def max_rel_err_complex(got, ref, den):
+    """Complex normalised error: max over elements of
+    max(|re(got - ref)|, |im(got - ref)|) / den (den: the 1-norm bound)."""
+    got = np.asarray(got, dtype=np.complex128)
+    d = np.maximum(np.abs(got.real - ref.real), np.abs(got.imag - ref.imag))
+    bad = (np.isnan(got.real) | np.isnan(got.imag)) & ~(np.isnan(ref.real) | np.isnan(ref.imag))
+    with np.errstate(divide="ignore", invalid="ignore"):
+        rel = np.where(den > 0, d / np.where(den > 0, den, 1.0), np.where(d == 0, 0.0, np.inf))
+    rel = np.where(bad, np.inf, rel)
+    return float(rel.max()) if rel.size else 0.0
 
 
 def is_small(transA, transB, M, N, K) -> bool:

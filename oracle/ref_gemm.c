@@ -133,6 +133,92 @@ int iaat_ref_gemm(int dtype, char transA, char transB,
 }
 
 /*
+ * iaat_ref_cgemm: the complex case (CGEMM / ZGEMM, Table I
+ * rows, PAPER.md:156-171 complex templates, Eq. 2), same
+ * definition over the complex field:
+ *   acc      = sum_k opA(i,k) * opB(k,j)          (complex, k ascending, double)
+ *   ref(i,j) = alpha*acc + beta*Cin(i,j)          (complex, double)
+ *   den(i,j) = |alpha|_1 * sum_k |opA|_1*|opB|_1 + |beta|_1*|Cin|_1
+ * where |x|_1 = |re x| + |im x| (a bound on every real product that enters
+ * either component).  op is transposition only (N or T; no conjugation,
+ * PAPER.md:101).  Elements are interleaved (re, im) pairs; ld's and strides
+ * count complex elements.  dtype: 2 = complex fp32, 3 = complex fp64.
+ * ref / den: packed, ref[2*(b*M*N + i + j*M) + {0,1}] = (re, im); den has
+ * one real per element.
+ */
+static void load_c(int dtype, const void *base, int64_t idx, double *re, double *im)
+{
+    if (dtype == 2) {
+        *re = (double)((const float *)base)[2 * idx];
+        *im = (double)((const float *)base)[2 * idx + 1];
+    } else {
+        *re = ((const double *)base)[2 * idx];
+        *im = ((const double *)base)[2 * idx + 1];
+    }
+}
+
+int iaat_ref_cgemm(int dtype, char transA, char transB,
+                   int64_t M, int64_t N, int64_t K, const double *alpha,
+                   const void *A, int64_t lda, int64_t strideA,
+                   const void *B, int64_t ldb, int64_t strideB,
+                   const double *beta, const void *Cin, int64_t ldc, int64_t strideC,
+                   int64_t batch, double *ref, double *den, int nthreads,
+                   int *threads_used)
+{
+    if (dtype != 2 && dtype != 3) return -1;
+    if (M < 0 || N < 0 || K < 0 || batch < 0) return -1;
+    const double ar = alpha[0], ai = alpha[1], br = beta[0], bi = beta[1];
+    const int beta_zero = (br == 0.0 && bi == 0.0), alpha_zero = (ar == 0.0 && ai == 0.0);
+    if (!beta_zero && Cin == NULL && M > 0 && N > 0) return -1;
+    const int tA = (transA == 'N' || transA == 'n') ? 0 : 1;
+    const int tB = (transB == 'N' || transB == 'n') ? 0 : 1;
+    int used = 1;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel
+    {
+#pragma omp single
+        used = omp_get_num_threads();
+    }
+#endif
+    if (threads_used) *threads_used = used;
+
+#pragma omp parallel for schedule(static)
+    for (int64_t b = 0; b < batch; ++b) {
+        const int64_t offA = b * strideA, offB = b * strideB, offC = b * strideC;
+        for (int64_t j = 0; j < N; ++j) {
+            for (int64_t i = 0; i < M; ++i) {
+                double sr = 0.0, si = 0.0, absacc = 0.0;
+                if (!alpha_zero) {                         /* reading A4 */
+                    for (int64_t k = 0; k < K; ++k) {      /* k ascending */
+                        double xr, xi, yr, yi;
+                        load_c(dtype, A, offA + (tA ? k + i * lda : i + k * lda), &xr, &xi);
+                        load_c(dtype, B, offB + (tB ? j + k * ldb : k + j * ldb), &yr, &yi);
+                        sr += xr * yr - xi * yi;           /* (x * y) re */
+                        si += xr * yi + xi * yr;           /* (x * y) im */
+                        absacc += (fabs(xr) + fabs(xi)) * (fabs(yr) + fabs(yi));
+                    }
+                }
+                double outr = ar * sr - ai * si, outi = ar * si + ai * sr;
+                double dd = (fabs(ar) + fabs(ai)) * absacc;
+                if (!beta_zero) {                          /* reading A3 */
+                    double cr, ci;
+                    load_c(dtype, Cin, offC + i + j * ldc, &cr, &ci);
+                    outr += br * cr - bi * ci;
+                    outi += br * ci + bi * cr;
+                    dd += (fabs(br) + fabs(bi)) * (fabs(cr) + fabs(ci));
+                }
+                const int64_t o = b * M * N + i + j * M;
+                ref[2 * o] = outr;
+                ref[2 * o + 1] = outi;
+                if (den) den[o] = dd;
+            }
+        }
+    }
+    return 0;
+}
+
+/*
  * Small-GEMM predicate, PAPER.md:36 (Sec. I): "cbrt(MNK) <= 80 when
  * transposition ... is not TN, or cbrt(MNK) <= 32 when ... TN", evaluated as
  * the integer test M*N*K <= 80^3 (32^3) (reading A10, inclusive).
