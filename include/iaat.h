@@ -17,9 +17,10 @@
  *      transB = 'N': B is K x N, ldb >= max(1, K);  'T': B is N x K, ldb >= max(1, N)
  *      C is M x N, ldc >= max(1, M).
  *    transA/transB are the characters 'N','n','T','t' (anything else,
- *    including 'C', is IAAT_ERROR_INVALID_VALUE: real types only).
+ *    including 'C', is IAAT_ERROR_INVALID_VALUE: transposition only).
  *  - alpha and beta are HOST pointers to one scalar of the call's dtype
- *    (float for IAAT_R32F, double for IAAT_R64F).
+ *    (float for IAAT_R32F, double for IAAT_R64F), or to two (re, im) for
+ *    IAAT_C32F (float[2]) / IAAT_C64F (double[2]).
  *  - A, B, C (and the pointer arrays of iaat_gemm_batched together with the
  *    matrices they point to) are DEVICE memory of the current CUDA device.
  *    The caller owns every buffer; the library keeps only a host-side plan
@@ -54,7 +55,11 @@
 extern "C" {
 #endif
 
-typedef enum { IAAT_R32F = 0, IAAT_R64F = 1 } iaat_dtype_t;
+/* Data types.  Complex (the paper's CGEMM / ZGEMM rows, PAPER.md:
+ * 96-97 Table I, Eq. 2): interleaved (re, im) element pairs,
+ * every ld / stride counts COMPLEX elements, alpha / beta point to two
+ * scalars (re, im); op is transposition only (N / T, no conjugation). */
+typedef enum { IAAT_R32F = 0, IAAT_R64F = 1, IAAT_C32F = 2, IAAT_C64F = 3 } iaat_dtype_t;
 
 typedef enum {
     IAAT_SUCCESS = 0,
@@ -107,6 +112,17 @@ iaat_status_t iaat_sgemm_batched(char transA, char transB, int64_t M, int64_t N,
 iaat_status_t iaat_dgemm_batched(char transA, char transB, int64_t M, int64_t N, int64_t K,
     double alpha, const double *const *Aarray, int64_t lda, const double *const *Barray,
     int64_t ldb, double beta, double *const *Carray, int64_t ldc, int64_t batch, void *stream);
+
+/* Complex typed wrappers: alpha / beta are host (re, im) pairs; A, B, C
+ * interleaved complex (float2 / double2 per element). */
+iaat_status_t iaat_cgemm_strided_batched(char transA, char transB, int64_t M, int64_t N,
+    int64_t K, const float alpha[2], const float *A, int64_t lda, int64_t strideA, const float *B,
+    int64_t ldb, int64_t strideB, const float beta[2], float *C, int64_t ldc, int64_t strideC,
+    int64_t batch, void *stream);
+iaat_status_t iaat_zgemm_strided_batched(char transA, char transB, int64_t M, int64_t N,
+    int64_t K, const double alpha[2], const double *A, int64_t lda, int64_t strideA, const double *B,
+    int64_t ldb, int64_t strideB, const double beta[2], double *C, int64_t ldc, int64_t strideC,
+    int64_t batch, void *stream);
 
 /* 1 if (transA, transB, M, N, K) is a small GEMM per PAPER.md:36, else 0.
  * Host only, no GPU needed.  Negative sizes -> 0.                          */

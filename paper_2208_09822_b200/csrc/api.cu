@@ -18,6 +18,7 @@
 
 #include "../../include/iaat.h"
 #include "iaat_device.cuh"
+#include "iaat_complex.cuh"
 #include "iaat_ks.cuh"
 #include "planner.h"
 
@@ -148,7 +149,7 @@ int64_t max1(int64_t x) { return x > 1 ? x : 1; }
 iaat_status_t validate(iaat_dtype_t dt, int ta, int tb, int64_t M, int64_t N, int64_t K, int64_t lda,
                        int64_t ldb, int64_t ldc, int64_t batch, const void *alpha, const void *beta)
 {
-    if (dt != IAAT_R32F && dt != IAAT_R64F) return IAAT_ERROR_INVALID_VALUE;
+    if (dt != IAAT_R32F && dt != IAAT_R64F && dt != IAAT_C32F && dt != IAAT_C64F) return IAAT_ERROR_INVALID_VALUE;
     if (ta < 0 || tb < 0) return IAAT_ERROR_INVALID_VALUE;
     if (M < 0 || N < 0 || K < 0 || batch < 0) return IAAT_ERROR_INVALID_VALUE;
     if (!alpha || !beta) return IAAT_ERROR_INVALID_VALUE;
@@ -162,8 +163,19 @@ iaat_status_t validate(iaat_dtype_t dt, int ta, int tb, int64_t M, int64_t N, in
 
 double scalar(iaat_dtype_t dt, const void *p)
 {
-    return dt == IAAT_R32F ? (double)*static_cast<const float *>(p) : *static_cast<const double *>(p);
+    return (dt == IAAT_R32F || dt == IAAT_C32F) ? (double)*static_cast<const float *>(p)
+                                                : *static_cast<const double *>(p);
 }
+
+// imaginary part of a complex alpha / beta (the second scalar); 0 for real dtypes
+double scalar_im(iaat_dtype_t dt, const void *p)
+{
+    if (dt == IAAT_C32F) return (double)static_cast<const float *>(p)[1];
+    if (dt == IAAT_C64F) return static_cast<const double *>(p)[1];
+    return 0.0;
+}
+
+int elt_bytes(iaat_dtype_t dt) { return dt == IAAT_R32F ? 4 : dt == IAAT_R64F ? 8 : dt == IAAT_C32F ? 8 : 16; }
 
 bool elem_aligned(const void *p, int elt) { return (reinterpret_cast<uintptr_t>(p) % elt) == 0; }
 
@@ -203,12 +215,18 @@ bool encode_tmap(CUtensorMap &m, const TmaGeo &g, const void *base, int elt)
 
 // alpha == 0 or K == 0 path: C = beta * C (or zeros).  A/B never read.
 iaat_status_t launch_scale(iaat_dtype_t dt, char *C, void *const *Carr, int64_t sC, int64_t M, int64_t N,
-                           int64_t ldc, int64_t batch, double beta, cudaStream_t s, int sm_count)
+                           int64_t ldc, int64_t batch, double beta, double beta_i, cudaStream_t s, int sm_count)
 {
     const int64_t total = M * N * batch;
     int64_t blocks = (total + 255) / 256;
     if (blocks > (int64_t)sm_count * 16) blocks = (int64_t)sm_count * 16;
-    if (dt == IAAT_R32F)
+    if (dt == IAAT_C32F)
+        cscale_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(C, Carr, sC, (int)M, (int)N, (int)ldc, batch, beta,
+                                                             beta_i);
+    else if (dt == IAAT_C64F)
+        cscale_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(C, Carr, sC, (int)M, (int)N, (int)ldc, batch, beta,
+                                                              beta_i);
+    else if (dt == IAAT_R32F)
         scale_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(C, Carr, sC, (int)M, (int)N, (int)ldc, batch, beta);
     else
         scale_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(C, Carr, sC, (int)M, (int)N, (int)ldc, batch, beta);
@@ -230,14 +248,15 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
     const int ta = parse_op(transA), tb = parse_op(transB);
     iaat_status_t st = validate(dt, ta, tb, M, N, K, lda, ldb, ldc, batch, alpha, beta);
     if (st != IAAT_SUCCESS) return st;
-    const int elt = dt == IAAT_R32F ? 4 : 8;
+    const int elt = elt_bytes(dt);
     if (!ptr_array && (sA < 0 || sB < 0 || sC < 0)) return IAAT_ERROR_INVALID_VALUE;
     // C problems must not overlap (reading A18)
     if (!ptr_array && batch > 1 && M > 0 && N > 0 && sC < (N - 1) * ldc + M) return IAAT_ERROR_INVALID_VALUE;
     if (M == 0 || N == 0 || batch == 0) return IAAT_SUCCESS;  // nothing to do (reading A5)
     const double a = scalar(dt, alpha), b = scalar(dt, beta);
-    const bool no_ab = (a == 0.0 || K == 0);
-    if (no_ab && b == 1.0) return IAAT_SUCCESS;  // C unchanged (reading A4)
+    const double ai = scalar_im(dt, alpha), bi = scalar_im(dt, beta);
+    const bool no_ab = ((a == 0.0 && ai == 0.0) || K == 0);
+    if (no_ab && b == 1.0 && bi == 0.0) return IAAT_SUCCESS;  // C unchanged (reading A4)
     if (ptr_array) {
         if (!Carr || (!no_ab && (!Aarr || !Barr))) return IAAT_ERROR_INVALID_VALUE;
     } else {
@@ -250,10 +269,10 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
     if (st != IAAT_SUCCESS) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (no_ab)
-        return launch_scale(dt, static_cast<char *>(C), Carr, sC, M, N, ldc, batch, b, s, dev.sm_count);
+        return launch_scale(dt, static_cast<char *>(C), Carr, sC, M, N, ldc, batch, b, bi, s, dev.sm_count);
 
     PlanRequest r;
-    r.dtype = dt == IAAT_R32F ? 0 : 1;
+    r.dtype = (int)dt;
     r.transA = ta;
     r.transB = tb;
     r.M = M;
@@ -266,7 +285,7 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
     r.sB = ptr_array ? 0 : sB;
     r.sC = ptr_array ? 0 : sC;
     r.batch = batch;
-    r.beta_zero = b == 0.0;
+    r.beta_zero = (b == 0.0 && bi == 0.0);
     r.alpha_zero = 0;
     uintptr_t orr = ptr_array ? 0 : (reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
                                      reinterpret_cast<uintptr_t>(C));
@@ -320,6 +339,8 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
     kp.Carr = Carr;
     kp.alpha = a;
     kp.beta = b;
+    kp.alpha_i = ai;
+    kp.beta_i = bi;
     LaunchFn fn = kLaunch[r.dtype][ta * 2 + tb][plan.vec];
     static const int smem_pad = std::getenv("IAAT_DEBUG_SMEM_PAD") ? std::atoi(std::getenv("IAAT_DEBUG_SMEM_PAD")) : 0;
     cudaError_t e = fn(kp, plan.grid, plan.block, std::min(plan.smem + smem_pad, IAAT_SMEM_LIMIT), s);
@@ -375,6 +396,24 @@ iaat_status_t iaat_dgemm_strided_batched(char transA, char transB, int64_t M, in
                                      strideB, &beta, C, ldc, strideC, batch, stream);
 }
 
+iaat_status_t iaat_cgemm_strided_batched(char transA, char transB, int64_t M, int64_t N, int64_t K,
+                                         const float alpha[2], const float *A, int64_t lda, int64_t strideA,
+                                         const float *B, int64_t ldb, int64_t strideB, const float beta[2], float *C,
+                                         int64_t ldc, int64_t strideC, int64_t batch, void *stream)
+{
+    return iaat_gemm_strided_batched(IAAT_C32F, transA, transB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
+                                     beta, C, ldc, strideC, batch, stream);
+}
+
+iaat_status_t iaat_zgemm_strided_batched(char transA, char transB, int64_t M, int64_t N, int64_t K,
+                                         const double alpha[2], const double *A, int64_t lda, int64_t strideA,
+                                         const double *B, int64_t ldb, int64_t strideB, const double beta[2],
+                                         double *C, int64_t ldc, int64_t strideC, int64_t batch, void *stream)
+{
+    return iaat_gemm_strided_batched(IAAT_C64F, transA, transB, M, N, K, alpha, A, lda, strideA, B, ldb, strideB,
+                                     beta, C, ldc, strideC, batch, stream);
+}
+
 iaat_status_t iaat_sgemm_batched(char transA, char transB, int64_t M, int64_t N, int64_t K, float alpha,
                                  const float *const *Aarray, int64_t lda, const float *const *Barray,
                                  int64_t ldb, float beta, float *const *Carray, int64_t ldc, int64_t batch,
@@ -416,7 +455,7 @@ iaat_status_t iaat_plan_describe(iaat_dtype_t dtype, char transA, char transB, i
     if (!json || cap == 0 || sm_count <= 0 || M == 0 || N == 0 || K == 0 || batch == 0)
         return IAAT_ERROR_INVALID_VALUE;
     PlanRequest r;
-    r.dtype = dtype == IAAT_R32F ? 0 : 1;
+    r.dtype = (int)dtype;
     r.transA = ta;
     r.transB = tb;
     r.M = M;

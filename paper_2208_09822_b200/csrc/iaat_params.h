@@ -59,6 +59,7 @@ struct IaatKParams {
     int64_t batch;       // problems in this call
     int64_t ngroups;     // ceil(batch / P)
     double alpha, beta;
+    double alpha_i, beta_i;  // imaginary parts (complex dtypes; 0 otherwise)
     int M, N, K;
     int lda, ldb, ldc;
     int P;               // problems per group (one pipeline stage)

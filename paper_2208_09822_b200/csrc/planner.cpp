@@ -40,6 +40,9 @@ namespace iaat {
 
 namespace {
 
+// element bytes of a dtype: 0 fp32, 1 fp64, 2 complex fp32, 3 complex fp64
+int elt_of(int dtype) { return dtype == 0 ? 4 : dtype == 1 ? 8 : dtype == 2 ? 8 : 16; }
+
 constexpr double kHbmBytesPerClk = 22.0;  // 6.5 TB/s / 148 SMs / ~2.0 GHz
 constexpr double kDfmaPerClk = 64.0;      // fp64 FMA lanes per SM per clock
 constexpr double kGroupOverhead = 150.0;  // mbarrier round trip + dispatch per group
@@ -401,7 +404,7 @@ Plan make_plan(const PlanRequest &r)
     kn.csmem = std::getenv("IAAT_FORCE_CSMEM") ? envi("IAAT_FORCE_CSMEM") : -1;
     bool tuned = false;
     if (!kn.any() && !r.ptr_array && !std::getenv("IAAT_NO_TUNING")) {
-        const int elt = r.dtype == 0 ? 4 : 8;
+        const int elt = elt_of(r.dtype);
         const int64_t colsA = r.transA ? r.M : r.K, colsB = r.transB ? r.K : r.N;
         const bool packed = r.batch <= 1 || (r.sA == r.lda * colsA && r.sB == r.ldb * colsB && r.sC == r.ldc * r.N);
         auto al16 = [&](int64_t el) { return (el * elt) % 16 == 0; };
@@ -440,7 +443,7 @@ Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn)
         return ksplan;
     }
     Plan plan;
-    const int elt = r.dtype == 0 ? 4 : 8;
+    const int elt = elt_of(r.dtype);
     const int vw = 16 / elt;
     const int tidx = r.transA * 2 + r.transB;
     const int64_t M = r.M, N = r.N, K = r.K;
@@ -621,6 +624,7 @@ Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn)
                     if (W > wmax) break;
                     double pipe = 0;
                     if (r.dtype == 1) pipe = (double)P * M * N * K / kDfmaPerClk;
+                    if (r.dtype == 3) pipe = 4.0 * P * M * N * K / kDfmaPerClk;  // 4 DFMA per complex MAC
                     Candidate c;
                     c.family = IAAT_FAM_FMA;
                     c.ms = ms;
@@ -824,7 +828,7 @@ void ks_class_cost(const PlanRequest &r, int elt, int mr, int nr, const Lanes &L
 
 bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
 {
-    if (r.ptr_array) return false;
+    if (r.ptr_array || r.dtype > 1) return false;  // complex types: slab family only
     const int elt = r.dtype == 0 ? 4 : 8;
     const int vw = 16 / elt, KU = vw, kc = 128 / elt;
     const int tidx = r.transA * 2 + r.transB;
@@ -1132,7 +1136,7 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
         s += buf;
     };
     add("\"status\": %d, \"dtype\": \"%s\", \"trans\": \"%c%c\", \"M\": %lld, \"N\": %lld, \"K\": %lld, ",
-        p.status, r.dtype ? "f64" : "f32", r.transA ? 'T' : 'N', r.transB ? 'T' : 'N', (long long)r.M,
+        p.status, r.dtype == 0 ? "f32" : r.dtype == 1 ? "f64" : r.dtype == 2 ? "c32" : "c64", r.transA ? 'T' : 'N', r.transB ? 'T' : 'N', (long long)r.M,
         (long long)r.N, (long long)r.K);
     if (p.status != 0) {
         s += "\"classes\": []}";

@@ -15,7 +15,7 @@ import os
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libiaat.so")
 
-IAAT_R32F, IAAT_R64F = 0, 1
+IAAT_R32F, IAAT_R64F, IAAT_C32F, IAAT_C64F = 0, 1, 2, 3
 STATUS = {
     0: "IAAT_SUCCESS",
     1: "IAAT_ERROR_INVALID_VALUE",
@@ -30,6 +30,7 @@ EXPORTS = [
     "iaat_gemm_strided_batched", "iaat_gemm_batched",
     "iaat_sgemm_strided_batched", "iaat_dgemm_strided_batched",
     "iaat_sgemm_batched", "iaat_dgemm_batched",
+    "iaat_cgemm_strided_batched", "iaat_zgemm_strided_batched",
     "iaat_is_small_gemm", "iaat_plan_describe", "iaat_catalog_describe",
     "iaat_status_string", "iaat_last_cuda_error", "iaat_launch_count", "iaat_version",
 ]
@@ -75,6 +76,13 @@ def _ch(x):
 
 
 def _scalar(dtype, v):
+    """Host scalar of the call's dtype; complex dtypes take (re, im) pairs."""
+    if dtype == IAAT_C32F:
+        v = complex(v)
+        return (ctypes.c_float * 2)(v.real, v.imag)
+    if dtype == IAAT_C64F:
+        v = complex(v)
+        return (ctypes.c_double * 2)(v.real, v.imag)
     return ctypes.byref(ctypes.c_float(v) if dtype == IAAT_R32F else ctypes.c_double(v))
 
 
@@ -148,7 +156,8 @@ def gemm_strided_batched(transA, transB, M, N, K, alpha, A, lda, strideA, B, ldb
     shape; only data_ptr() is used).  Raises IaatError on a non-success
     status when check=True."""
     import torch
-    dtype = {torch.float32: IAAT_R32F, torch.float64: IAAT_R64F}[C.dtype]
+    dtype = {torch.float32: IAAT_R32F, torch.float64: IAAT_R64F, torch.complex64: IAAT_C32F,
+             torch.complex128: IAAT_C64F}[C.dtype]
     st = iaat_gemm_strided_batched(dtype, transA, transB, M, N, K, alpha, A.data_ptr(), lda, strideA,
                                    B.data_ptr(), ldb, strideB, beta, C.data_ptr(), ldc, strideC, batch,
                                    _stream_handle(stream))

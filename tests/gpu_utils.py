@@ -129,3 +129,78 @@ def config4_shapes():
 
 def config2_batch(n, elt=4):
     return (256 * 1024 * 1024) // ((3 * n * n) * elt)
+
+
+# ---------------------------------------------------------------- complex
+CTOL = {np.complex64: 1e-5, np.complex128: 1e-13}
+
+
+class CCase:
+    """One strided-batched complex problem set on the GPU.  Interleaved
+    (re, im) data are generated as a real (2*rows) x cols matrix with real
+    ld 2*ld by the same counter generator (no new generator arithmetic)."""
+
+    def __init__(self, cdtype, tA, tB, M, N, K, batch, seed, alpha, beta, pad=0, spad=0):
+        import torch
+        self.cdtype, self.tA, self.tB = cdtype, tA, tB
+        self.rdtype = np.float32 if cdtype == np.complex64 else np.float64
+        self.M, self.N, self.K, self.batch, self.seed = M, N, K, batch, seed
+        self.alpha, self.beta = complex(alpha), complex(beta)
+        ra, ca = stored(tA, M, K)
+        rb, cb = stored(tB, K, N)
+        self.ra, self.ca, self.rb, self.cb = ra, ca, rb, cb
+        self.lda, self.ldb, self.ldc = max(1, ra) + pad, max(1, rb) + pad, max(1, M) + pad
+        self.sA, self.sB, self.sC = self.lda * ca + spad, self.ldb * cb + spad, self.ldc * N + spad
+        tdt = torch.float32 if self.rdtype == np.float32 else torch.float64
+        self.A = torch.full((2 * (batch * self.sA + 8),), float("nan"), dtype=tdt, device="cuda")
+        self.B = torch.full((2 * (batch * self.sB + 8),), float("nan"), dtype=tdt, device="cuda")
+        self.C = torch.full((2 * (batch * self.sC + 8),), float("nan"), dtype=tdt, device="cuda")
+        if batch:
+            datagen.fill_device(self.A, seed, datagen.MAT_A, 2 * ra, ca, 2 * self.lda, 2 * self.sA, batch)
+            datagen.fill_device(self.B, seed, datagen.MAT_B, 2 * rb, cb, 2 * self.ldb, 2 * self.sB, batch)
+            datagen.fill_device(self.C, seed, datagen.MAT_C, 2 * M, N, 2 * self.ldc, 2 * self.sC, batch)
+
+    def run(self, check=True):
+        from paper_2208_09822_b200 import iaat
+        dt = iaat.IAAT_C32F if self.cdtype == np.complex64 else iaat.IAAT_C64F
+        st = iaat.iaat_gemm_strided_batched(dt, self.tA, self.tB, self.M, self.N, self.K, self.alpha,
+                                            self.A.data_ptr(), self.lda, self.sA, self.B.data_ptr(), self.ldb,
+                                            self.sB, self.beta, self.C.data_ptr(), self.ldc, self.sC, self.batch)
+        if check and st != 0:
+            raise iaat.IaatError(st)
+        return st
+
+    def host(self, mat, rows, cols, ld, ids):
+        re = datagen.fill_host(self.seed, mat, self.rdtype, 2 * rows, cols, 2 * ld, 2 * ld * cols, ids)
+        return re.view(self.cdtype)
+
+    def oracle(self, ids):
+        ids = np.asarray(ids, dtype=np.int64)
+        A = self.host(datagen.MAT_A, self.ra, self.ca, self.lda, ids)
+        B = self.host(datagen.MAT_B, self.rb, self.cb, self.ldb, ids)
+        C = self.host(datagen.MAT_C, self.M, self.N, self.ldc, ids)
+        ref, den, _ = oracle.ref_cgemm(self.tA, self.tB, self.M, self.N, self.K, self.alpha, A, self.lda,
+                                       self.lda * self.ca, B, self.ldb, self.ldb * self.cb, self.beta, C, self.ldc,
+                                       self.ldc * self.N, len(ids))
+        return ref, den
+
+    def gpu_result(self, ids):
+        import torch
+        C = self.C.view(-1, 2)
+        ids = torch.as_tensor(np.asarray(ids, dtype=np.int64), device=C.device)
+        j = torch.arange(self.N, device=C.device).view(1, -1, 1) * self.ldc
+        i = torch.arange(self.M, device=C.device).view(1, 1, -1)
+        idx = ids.view(-1, 1, 1) * self.sC + j + i
+        v = C[idx].double().cpu().numpy()
+        return v[..., 0] + 1j * v[..., 1]
+
+    def check(self, ids=None, tol=None):
+        if ids is None:
+            ids = np.arange(self.batch)
+        ref, den = self.oracle(ids)
+        got = self.gpu_result(ids)
+        err = oracle.max_rel_err_complex(got, ref, den)
+        tol = CTOL[self.cdtype] if tol is None else tol
+        assert err <= tol, "complex max rel err %.3e > %.1e (%s%s M=%d N=%d K=%d)" % (
+            err, tol, self.tA, self.tB, self.M, self.N, self.K)
+        return err
