@@ -62,7 +62,15 @@ class Shape:
 
     @property
     def elt(self):
-        return 4 if self.dtype == "f32" else 8
+        return {"f32": 4, "f64": 8, "c32": 8, "c64": 16}[self.dtype]
+
+    @property
+    def cplx(self):
+        return self.dtype in ("c32", "c64")
+
+    @property
+    def dt_index(self):
+        return {"f32": 0, "f64": 1, "c32": 2, "c64": 3}[self.dtype]
 
     def stored(self):
         ra, ca = (self.M, self.K) if self.tr[0] == "N" else (self.K, self.M)
@@ -70,7 +78,8 @@ class Shape:
         return ra, ca, rb, cb
 
     def flops(self, batch=None):
-        return 2.0 * self.M * self.N * self.K * (self.batch if batch is None else batch)
+        # Eq. 1 (real) / Eq. 2 (complex: 8 flops per complex multiply-add)
+        return (8.0 if self.cplx else 2.0) * self.M * self.N * self.K * (self.batch if batch is None else batch)
 
     def alg_bytes(self, batch=None):
         b = self.batch if batch is None else batch
@@ -112,6 +121,20 @@ def workload(cfg):
             for tr in ("NN", "NT"):
                 S.append(Shape("f64", tr, n, n, n, 2_000_000, 1.0, 0.0, 4))
         desc = "config5: fp64 NN/NT M=N=K in {8,16,32,48,64,80}, batch 2e6 (chunked to fit HBM), alpha=1, beta=0"
+    elif cfg == 6:  # SURVEY f1 (not a BASELINE config): complex fp32, config-2 shape of sweep
+        for n in range(4, 81, 4):
+            b = (256 * 1024 * 1024) // (3 * n * n * 8)
+            for tr in ("NN", "NT", "TT"):
+                S.append(Shape("c32", tr, n, n, n, b, 1.5 - 0.5j, 0.5 + 0.25j, 1))
+        desc = ("cgemm sweep (SURVEY f1): complex fp32 M=N=K in {4,...,80} x {NN,NT,TT}, batch=floor(256MiB/(3n^2*8B)), "
+                "alpha=1.5-0.5i, beta=0.5+0.25i, seed 1; GFLOP/s by Eq. 2 (8MNK)")
+    elif cfg == 7:  # complex fp64
+        for n in (8, 16, 24, 32, 40, 48):
+            b = (256 * 1024 * 1024) // (3 * n * n * 16)
+            for tr in ("NN", "NT", "TT"):
+                S.append(Shape("c64", tr, n, n, n, b, 1.5 - 0.5j, 0.5 + 0.25j, 1))
+        desc = ("zgemm sweep (SURVEY f1): complex fp64 M=N=K in {8,...,48} x {NN,NT,TT}, batch=floor(256MiB/(3n^2*16B)), "
+                "alpha=1.5-0.5i, beta=0.5+0.25i, seed 1; GFLOP/s by Eq. 2 (8MNK)")
     else:
         raise SystemExit("unknown config %r" % cfg)
     return S, desc
@@ -180,7 +203,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     shapes, desc = workload(args.config)
     stream = torch.cuda.current_stream()
-    tdt = {"f32": torch.float32, "f64": torch.float64}
+    tdt = {"f32": torch.float32, "f64": torch.float64, "c32": torch.float32, "c64": torch.float64}
 
     # --- allocate + fill (outside the timed region); one buffer set per (dtype, M,N,K)
     hbm_cap = torch.cuda.get_device_properties(dev).total_memory
@@ -202,13 +225,14 @@ def run_ours(args, rank, world, local_rank):
             bufs.clear()
             torch.cuda.empty_cache()
         ra, ca, rb, cb = s.stored()
-        A = torch.empty(cnt * ra * ca, dtype=tdt[s.dtype], device=dev)
-        B = torch.empty(cnt * rb * cb, dtype=tdt[s.dtype], device=dev)
-        C = torch.empty(cnt * s.M * s.N, dtype=tdt[s.dtype], device=dev)
+        w = 2 if s.cplx else 1  # complex: interleaved (re, im) = a real (2*rows) x cols matrix
+        A = torch.empty(w * cnt * ra * ca, dtype=tdt[s.dtype], device=dev)
+        B = torch.empty(w * cnt * rb * cb, dtype=tdt[s.dtype], device=dev)
+        C = torch.empty(w * cnt * s.M * s.N, dtype=tdt[s.dtype], device=dev)
         first = rank * s.batch + lo  # global problem ids: ranks own disjoint problems
-        datagen.fill_device(A, s.seed, datagen.MAT_A, ra, ca, ra, ra * ca, cnt, first)
-        datagen.fill_device(B, s.seed, datagen.MAT_B, rb, cb, rb, rb * cb, cnt, first)
-        datagen.fill_device(C, s.seed, datagen.MAT_C, s.M, s.N, s.M, s.M * s.N, cnt, first)
+        datagen.fill_device(A, s.seed, datagen.MAT_A, w * ra, ca, w * ra, w * ra * ca, cnt, first)
+        datagen.fill_device(B, s.seed, datagen.MAT_B, w * rb, cb, w * rb, w * rb * cb, cnt, first)
+        datagen.fill_device(C, s.seed, datagen.MAT_C, w * s.M, s.N, w * s.M, w * s.M * s.N, cnt, first)
         bufs[key] = (A, B, C)
         if args.config == 5:
             break  # config 5 re-fills per chunk inside the step loop (generation untimed, see below)
@@ -218,7 +242,7 @@ def run_ours(args, rank, world, local_rank):
     def call(s, lo, cnt):
         ra, ca, rb, cb = s.stored()
         A, B, C = bufs[(s.dtype, s.M, s.N, s.K, s.tr, cnt)]
-        st = iaat.iaat_gemm_strided_batched(0 if s.dtype == "f32" else 1, s.tr[0], s.tr[1], s.M, s.N, s.K,
+        st = iaat.iaat_gemm_strided_batched(s.dt_index, s.tr[0], s.tr[1], s.M, s.N, s.K,
                                             s.alpha, A.data_ptr(), ra, ra * ca, B.data_ptr(), rb, rb * cb,
                                             s.beta, C.data_ptr(), s.M, s.M * s.N, cnt, stream.cuda_stream)
         if st != 0:
@@ -274,7 +298,7 @@ def run_ours(args, rank, world, local_rank):
     for i, (s, lo, cnt) in enumerate(chunks):
         t = per_call_ms[i] * 1e-3
         gf = s.flops(cnt) / t / 1e9
-        t_roof = max(s.flops(cnt) / (FFMA_PEAK_TFLOPS * 1e12 if s.dtype == "f32" else DMMA_PEAK_TFLOPS * 1e12),
+        t_roof = max(s.flops(cnt) / (FFMA_PEAK_TFLOPS * 1e12 if s.dtype in ("f32", "c32") else DMMA_PEAK_TFLOPS * 1e12),
                      s.alg_bytes(cnt) / (pk["hbm_gbs"] * 1e9))
         shapes_out.append({"shape": s.name(), "batch": cnt, "us": round(t * 1e6, 2), "gflops": round(gf, 1),
                            "hbm_gbs": round(s.alg_bytes(cnt) / t / 1e9, 1),
@@ -282,7 +306,7 @@ def run_ours(args, rank, world, local_rank):
     s, lo, cnt = chunks[dom]
     tdom = per_call_ms[dom] * 1e-3
     hbm_time = s.alg_bytes(cnt) / (pk["hbm_gbs"] * 1e9)
-    cmp_peak = FFMA_PEAK_TFLOPS if s.dtype == "f32" else DMMA_PEAK_TFLOPS
+    cmp_peak = FFMA_PEAK_TFLOPS if s.dtype in ("f32", "c32") else DMMA_PEAK_TFLOPS
     cmp_time = s.flops(cnt) / (cmp_peak * 1e12)
     traffic = load_traffic(s.name())
     if hbm_time >= cmp_time:
@@ -307,7 +331,7 @@ def run_ours(args, rank, world, local_rank):
     line = {"metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32" if shapes[0].dtype == "f32" else "f64", "data": "synthetic",
+            "dtype": shapes[0].dtype, "data": "synthetic",
             "config": {"workload": desc, "calls_per_step": len(chunks),
                        "l2": "inputs larger than L2: every call streams its own 256 MiB operand set "
                              "(126 MB L2), no flush kernel needed" if args.config == 2 else
@@ -431,23 +455,28 @@ def oracle_sample(shapes, frac):
 def run_oracle_timed(shapes, frac, repeats=1):
     import datagen
     import oracle
-    dt = {"f32": np.float32, "f64": np.float64}
+    dt = {"f32": np.float32, "f64": np.float64, "c32": np.float32, "c64": np.float64}
+    cdt = {"c32": np.complex64, "c64": np.complex128}
     sample = oracle_sample(shapes, frac)
     inputs = []
     for s, n in sample:
         ra, ca, rb, cb = s.stored()
         ids = np.arange(n)
-        A = datagen.fill_host(s.seed, 0, dt[s.dtype], ra, ca, ra, ra * ca, ids)
-        B = datagen.fill_host(s.seed, 1, dt[s.dtype], rb, cb, rb, rb * cb, ids)
-        C = datagen.fill_host(s.seed, 2, dt[s.dtype], s.M, s.N, s.M, s.M * s.N, ids)
+        w = 2 if s.cplx else 1
+        A = datagen.fill_host(s.seed, 0, dt[s.dtype], w * ra, ca, w * ra, w * ra * ca, ids)
+        B = datagen.fill_host(s.seed, 1, dt[s.dtype], w * rb, cb, w * rb, w * rb * cb, ids)
+        C = datagen.fill_host(s.seed, 2, dt[s.dtype], w * s.M, s.N, w * s.M, w * s.M * s.N, ids)
+        if s.cplx:
+            A, B, C = A.view(cdt[s.dtype]), B.view(cdt[s.dtype]), C.view(cdt[s.dtype])
         inputs.append((s, n, A, B, C))
     total_t, total_f, threads = 0.0, 0.0, 0
     for _ in range(repeats):
         for s, n, A, B, C in inputs:
             ra, ca, rb, cb = s.stored()
             t = time.perf_counter()
-            _, _, threads = oracle.ref_gemm(s.tr[0], s.tr[1], s.M, s.N, s.K, s.alpha, A, ra, ra * ca, B, rb,
-                                            rb * cb, s.beta, C, s.M, s.M * s.N, n, want_den=False)
+            fn = oracle.ref_cgemm if s.cplx else oracle.ref_gemm
+            _, _, threads = fn(s.tr[0], s.tr[1], s.M, s.N, s.K, s.alpha, A, ra, ra * ca, B, rb,
+                               rb * cb, s.beta, C, s.M, s.M * s.N, n, want_den=False)
             total_t += time.perf_counter() - t
             total_f += s.flops(n)
     return total_f / total_t / 1e9, threads, total_t
@@ -540,7 +569,8 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=2,
+                    help="BASELINE.json configs 1-5; 6/7 = complex fp32/fp64 sweeps (SURVEY f1)")
     ap.add_argument("--cpu-frac", type=float, default=0.5)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")

@@ -55,6 +55,14 @@ def config_shapes(cfg):
         for n in (8, 16, 32, 48, 64, 80):
             for tr in ("NN", "NT"):
                 out.append(("f64", tr, n, n, n, 2_000_000, 1.0, 0.0))
+    elif cfg == 6:  # complex fp32 sweep (bench.py --config 6)
+        for n in range(4, 81, 4):
+            for tr in ("NN", "NT", "TT"):
+                out.append(("c32", tr, n, n, n, (256 << 20) // (24 * n * n), 1.5 - 0.5j, 0.5 + 0.25j))
+    elif cfg == 7:  # complex fp64 sweep (bench.py --config 7)
+        for n in (8, 16, 24, 32, 40, 48):
+            for tr in ("NN", "NT", "TT"):
+                out.append(("c64", tr, n, n, n, (256 << 20) // (48 * n * n), 1.5 - 0.5j, 0.5 + 0.25j))
     return out
 
 
@@ -77,24 +85,25 @@ class Bench:
         import torch
         import datagen
         self.torch = torch
-        self.dt = 0 if dtype == "f32" else 1
-        elt = 4 if dtype == "f32" else 8
+        self.dt = {"f32": 0, "f64": 1, "c32": 2, "c64": 3}[dtype]
+        elt = {"f32": 4, "f64": 8, "c32": 8, "c64": 16}[dtype]
+        w = 2 if dtype in ("c32", "c64") else 1  # complex: interleaved (re, im) pairs
         self.tr, self.M, self.N, self.K, self.alpha, self.beta = tr, M, N, K, alpha, beta
         ra, ca = (M, K) if tr[0] == "N" else (K, M)
         rb, cb = (K, N) if tr[1] == "N" else (N, K)
         per = (ra * ca + rb * cb + M * N) * elt
         self.batch = int(min(batch, max(1, max_bytes // per)))
         self.ra, self.ca, self.rb, self.cb = ra, ca, rb, cb
-        tdt = torch.float32 if elt == 4 else torch.float64
+        tdt = torch.float32 if dtype in ("f32", "c32") else torch.float64
         nsets = self.NSETS if self.batch * per < (1 << 30) else 1
         self.sets = []
         for i in range(nsets):
-            A = torch.empty(self.batch * ra * ca, dtype=tdt, device="cuda")
-            B = torch.empty(self.batch * rb * cb, dtype=tdt, device="cuda")
-            C = torch.empty(self.batch * M * N, dtype=tdt, device="cuda")
-            datagen.fill_device(A, 9 + i, 0, ra, ca, ra, ra * ca, self.batch)
-            datagen.fill_device(B, 9 + i, 1, rb, cb, rb, rb * cb, self.batch)
-            datagen.fill_device(C, 9 + i, 2, M, N, M, M * N, self.batch)
+            A = torch.empty(w * self.batch * ra * ca, dtype=tdt, device="cuda")
+            B = torch.empty(w * self.batch * rb * cb, dtype=tdt, device="cuda")
+            C = torch.empty(w * self.batch * M * N, dtype=tdt, device="cuda")
+            datagen.fill_device(A, 9 + i, 0, w * ra, ca, w * ra, w * ra * ca, self.batch)
+            datagen.fill_device(B, 9 + i, 1, w * rb, cb, w * rb, w * rb * cb, self.batch)
+            datagen.fill_device(C, 9 + i, 2, w * M, N, w * M, w * M * N, self.batch)
             self.sets.append((A, B, C))
         self.turn = 0
 
@@ -148,7 +157,7 @@ def tile_options(M, N):
 
 def tune_shape(sh, log):
     dtype, tr, M, N, K, batch, alpha, beta = sh
-    elt = 4 if dtype == "f32" else 8
+    elt = {"f32": 4, "f64": 8, "c32": 8, "c64": 16}[dtype]
     b = Bench(*sh)
     results = []  # (us, knobs dict)
 
@@ -215,9 +224,9 @@ def tune_shape(sh, log):
     if auto is not None and auto <= best_us * 1.01:
         best_kw, best_us = {}, auto
     byts = (M * K + K * N + M * N * (1 if beta == 0 else 2)) * elt * b.batch
+    fl = (8.0 if dtype in ("c32", "c64") else 2.0) * M * N * K * b.batch
     log("%s %s %dx%dx%d batch=%d auto=%.1fus best=%.1fus (%.0f GB/s, %.0f GFLOP/s) knobs=%s" % (
-        dtype, tr, M, N, K, b.batch, auto or -1, best_us, byts / best_us / 1e3,
-        2.0 * M * N * K * b.batch / best_us / 1e3, best_kw))
+        dtype, tr, M, N, K, b.batch, auto or -1, best_us, byts / best_us / 1e3, fl / best_us / 1e3, best_kw))
     return best_kw, best_p
 
 
@@ -260,7 +269,7 @@ def main(argv=None):
                 continue
             kw, p = tune_shape(sh, log)
             dtype, tr, M, N, K, batch, alpha, beta = sh
-            key = key_line(0 if dtype == "f32" else 1, tr, M, N, K, beta == 0)
+            key = key_line({"f32": 0, "f64": 1, "c32": 2, "c64": 3}[dtype], tr, M, N, K, beta == 0)
             if kw:
                 existing[key] = knobs_to_line(kw, p)
             else:
