@@ -140,6 +140,14 @@ iaat_status_t iaat_plan_describe(
     int64_t batch, int beta_is_zero, int alpha_is_zero, int64_t base_align_bytes,
     int sm_count, char *json, size_t cap);
 
+/* Host only (an ablation of the GPU planner): the paper's own
+ * tiling of an SGEMM_NN M x N block with the Table I catalog
+ * and the memops cost (m_0+n_0+...)K + 2MN as JSON:
+ * mode 0 = Alg. 2 traced literally (readings DESIGN.md
+ * A14), mode 1 = the exact optimum over Table I (Fig. 2's 72K+450 for
+ * 15 x 15).  1 <= M, N <= 4096.                              */
+iaat_status_t iaat_paper_tile(int mode, int64_t M, int64_t N, char *json, size_t cap);
+
 /* Static description of the install-time kernel catalog as JSON. */
 iaat_status_t iaat_catalog_describe(char *json, size_t cap);
 

@@ -489,6 +489,15 @@ iaat_status_t iaat_catalog_describe(char *json, size_t cap)
     return IAAT_SUCCESS;
 }
 
+iaat_status_t iaat_paper_tile(int mode, int64_t M, int64_t N, char *json, size_t cap)
+{
+    if ((mode != 0 && mode != 1) || M < 1 || N < 1 || M > 4096 || N > 4096 || !json) return IAAT_ERROR_INVALID_VALUE;
+    const std::string s = paper_tile_json(mode, (int)M, (int)N);
+    if (s.size() + 1 > cap) return IAAT_ERROR_INVALID_VALUE;
+    std::memcpy(json, s.c_str(), s.size() + 1);
+    return IAAT_SUCCESS;
+}
+
 const char *iaat_status_string(iaat_status_t s)
 {
     switch (s) {

@@ -1182,4 +1182,200 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
     return s;
 }
 
+
+// ============================================================================
+// Paper-faithful tiling mode (an ablation baseline for the GPU
+// planner, host only).  The SGEMM_NN kernel catalog of Table I (PAPER.md:94,
+// the NN column of the SGEMM row) and the run-time tile algorithm of Sec.
+// V-A (Alg. 2) with its memops cost "(m_0 + n_0 + ... +
+// m_a + n_a) K + 2mn".
+//   mode 0: Alg. 2 traced literally, with the readings of DESIGN.md A14:
+//           ExtendTo8/16(m1) regroup the 4-high strips into 8-/16-high ones
+//           (remainder stays 4); "tile N by m8[] / m16[]" = TileSingleDim(N,
+//           widths allowed for that height); TileSingleDim is greedy
+//           largest-first and averages the last two pieces when the
+//           remainder is below half the largest width (the threshold of
+//           PAPER.md:319 is unstated).
+//   mode 1: the exact optimum over Table I: row strips of catalog heights,
+//           each strip tiled in N by its widest allowed width (a strip of
+//           height h costs ceil(N / w_max(h)) * h + N), dynamic programming
+//           over M -- the decomposition behind Fig. 2's 72K + 450 for 15 x 15
+//           (PAPER.md:337).
+// ============================================================================
+namespace paper {
+
+struct Piece {
+    int dim, nums;
+};
+struct StripPlan {
+    int h, count;
+    std::vector<Piece> n;  // widths of one strip
+};
+
+// Table I, SGEMM NN: m_c -> the largest n_c (every n_c from 1 up is generated)
+int nmax_nn(int mc)
+{
+    switch (mc) {
+    case 16: return 4;
+    case 12: return 6;
+    case 8: return 8;
+    case 4: case 3: case 2: case 1: return 13;
+    }
+    return 0;
+}
+
+// TileSingleDim(D, sizes): (dim, nums) pairs, largest first
+std::vector<Piece> tile_single_dim(int D, const std::vector<int> &sizes)
+{
+    int big = 0;
+    for (int s : sizes) big = std::max(big, s);
+    std::vector<Piece> out;
+    if (D <= 0 || big <= 0) return out;
+    const int q = D / big, r = D % big;
+    if (q > 0) out.push_back({big, q});
+    if (r > 0) {
+        if (q > 0 && 2 * r < big) {
+            // average the last two pieces: big + r -> two near-equal widths
+            const int a = (big + r + 1) / 2, b = (big + r) / 2;
+            if (out.back().nums == 1) out.pop_back(); else out.back().nums -= 1;
+            out.push_back({a, 1});
+            if (b > 0) out.push_back({b, 1});
+        } else {
+            out.push_back({r, 1});
+        }
+    }
+    return out;
+}
+
+std::vector<int> range1(int hi)
+{
+    std::vector<int> v;
+    for (int i = 1; i <= hi; ++i) v.push_back(i);
+    return v;
+}
+
+int64_t strips_cost(const std::vector<StripPlan> &s)
+{
+    int64_t c = 0;
+    for (const auto &p : s)
+        for (const auto &w : p.n) c += (int64_t)p.count * w.nums * (p.h + w.dim);
+    return c;
+}
+
+// ExtendTo8 / ExtendTo16 of m1 = (4, q): regroup 4-strips into e-high strips
+std::vector<StripPlan> extend(int q, int e, int N)
+{
+    std::vector<StripPlan> v;
+    const int per = e / 4, big = q / per, rem = q % per;
+    if (big > 0) v.push_back({e, big, tile_single_dim(N, range1(nmax_nn(e)))});
+    if (rem > 0) v.push_back({4, rem, tile_single_dim(N, range1(nmax_nn(4)))});
+    return v;
+}
+
+std::vector<StripPlan> alg2_literal(int M, int N)
+{
+    std::vector<StripPlan> s;
+    if (N <= 13) {
+        // lines 1-7: n_c = N, m_1 the largest m_c whose kernel has n_c = N
+        int m1 = 1;
+        for (int mc : {16, 12, 8, 4, 3, 2, 1})
+            if (nmax_nn(mc) >= N && mc <= M) {
+                m1 = mc;
+                break;
+            }
+        const int I = M / m1;
+        s.push_back({m1, I, {{N, 1}}});
+        // line 5 appends (M - m_1 I, 1); a remainder with no kernel of its
+        // own height (5, 6, 7, 9, 10, 11, 13-15) is split into Table I
+        // heights largest-first (reading A14)
+        for (int rem = M - m1 * I; rem > 0;) {
+            int h = 1;
+            for (int mc : {16, 12, 8, 4, 3, 2, 1})
+                if (mc <= rem && nmax_nn(mc) >= N) {
+                    h = mc;
+                    break;
+                }
+            s.push_back({h, 1, {{N, 1}}});
+            rem -= h;
+        }
+        return s;
+    }
+    const std::vector<int> w13 = range1(13), w8 = range1(8), w6 = range1(6);
+    if (M < 8) {
+        for (const Piece &p : tile_single_dim(M, {1, 2, 3, 4})) s.push_back({p.dim, p.nums, tile_single_dim(N, w13)});
+    } else if (M == 9) {
+        for (int h : {4, 3, 2}) s.push_back({h, 1, tile_single_dim(N, w13)});
+    } else if (M < 12) {
+        s.push_back({8, 1, tile_single_dim(N, w8)});
+        if (M > 8) s.push_back({M - 8, 1, tile_single_dim(N, w13)});  // (M-8, 1) is empty at M == 8 (reading A14)
+    } else if (M == 12) {
+        s.push_back({12, 1, tile_single_dim(N, w6)});
+    } else {
+        int q = M / 4;
+        std::vector<StripPlan> m2;
+        if (M - 4 * q == 1) {
+            q -= 1;
+            m2.push_back({3, 1, tile_single_dim(N, w8)});
+            m2.push_back({2, 1, tile_single_dim(N, w13)});
+        } else if (M - 4 * q > 0) {
+            m2.push_back({M - 4 * q, 1, tile_single_dim(N, w13)});
+        }
+        std::vector<StripPlan> b8 = extend(q, 8, N), b16 = extend(q, 16, N);
+        s = strips_cost(b16) < strips_cost(b8) ? b16 : b8;  // CompareLessMemops
+        for (auto &p : m2) s.push_back(p);
+    }
+    return s;
+}
+
+std::vector<StripPlan> optimal(int M, int N)
+{
+    const int H[] = {16, 12, 8, 4, 3, 2, 1};
+    std::vector<int64_t> best(M + 1, (int64_t)1 << 60);
+    std::vector<int> pick(M + 1, 0);
+    best[0] = 0;
+    for (int m = 1; m <= M; ++m)
+        for (int h : H) {
+            if (h > m) continue;
+            const int64_t c = best[m - h] + (int64_t)((N + nmax_nn(h) - 1) / nmax_nn(h)) * h + N;
+            if (c < best[m]) {  // ties: the first (larger) height wins
+                best[m] = c;
+                pick[m] = h;
+            }
+        }
+    std::vector<StripPlan> s;
+    for (int m = M; m > 0; m -= pick[m]) {
+        const int h = pick[m], w = nmax_nn(h);
+        std::vector<Piece> n;
+        if (N / w) n.push_back({w, N / w});
+        if (N % w) n.push_back({N % w, 1});
+        if (!s.empty() && s.back().h == h) s.back().count += 1;
+        else s.push_back({h, 1, n});
+    }
+    return s;
+}
+
+}  // namespace paper
+
+std::string paper_tile_json(int mode, int M, int N)
+{
+    std::vector<paper::StripPlan> s = mode == 0 ? paper::alg2_literal(M, N) : paper::optimal(M, N);
+    std::string j = "{\"mode\": \"";
+    j += mode == 0 ? "alg2_literal" : "table1_optimal";
+    j += "\", \"strips\": [";
+    char buf[128];
+    for (size_t i = 0; i < s.size(); ++i) {
+        std::snprintf(buf, sizeof buf, "%s{\"h\": %d, \"count\": %d, \"n\": [", i ? ", " : "", s[i].h, s[i].count);
+        j += buf;
+        for (size_t k = 0; k < s[i].n.size(); ++k) {
+            std::snprintf(buf, sizeof buf, "%s[%d, %d]", k ? ", " : "", s[i].n[k].dim, s[i].n[k].nums);
+            j += buf;
+        }
+        j += "]}";
+    }
+    std::snprintf(buf, sizeof buf, "], \"memops_k_coeff\": %lld, \"memops_const\": %lld}",
+                  (long long)paper::strips_cost(s), (long long)2 * M * N);
+    j += buf;
+    return j;
+}
+
 }  // namespace iaat

@@ -68,4 +68,8 @@ bool catalog_has(int dtype, int trans_idx, int family, int mr, int nr);
 int catalog_code(int family, int mr, int nr);
 const char *catalog_json();
 
+// Paper-faithful tiling of an SGEMM_NN M x N block with the Table I catalog
+// (SURVEY f3): mode 0 = Alg. 2 literal, 1 = optimal DP; JSON.
+std::string paper_tile_json(int mode, int M, int N);
+
 }  // namespace iaat

@@ -31,7 +31,7 @@ EXPORTS = [
     "iaat_sgemm_strided_batched", "iaat_dgemm_strided_batched",
     "iaat_sgemm_batched", "iaat_dgemm_batched",
     "iaat_cgemm_strided_batched", "iaat_zgemm_strided_batched",
-    "iaat_is_small_gemm", "iaat_plan_describe", "iaat_catalog_describe",
+    "iaat_is_small_gemm", "iaat_plan_describe", "iaat_catalog_describe", "iaat_paper_tile",
     "iaat_status_string", "iaat_last_cuda_error", "iaat_launch_count", "iaat_version",
 ]
 
@@ -58,6 +58,8 @@ def _load():
     lib.iaat_plan_describe.argtypes = [i, c, c, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i, i,
                                        i64, i, ctypes.c_char_p, ctypes.c_size_t]
     lib.iaat_plan_describe.restype = i
+    lib.iaat_paper_tile.argtypes = [i, i64, i64, ctypes.c_char_p, ctypes.c_size_t]
+    lib.iaat_paper_tile.restype = i
     lib.iaat_catalog_describe.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
     lib.iaat_catalog_describe.restype = i
     lib.iaat_status_string.argtypes = [i]
@@ -115,6 +117,15 @@ def iaat_plan_describe(dtype, transA, transB, M, N, K, lda, strideA, ldb, stride
                                  sm_count, buf, len(buf))
     if st != 0:
         raise IaatError(st, "iaat_plan_describe")
+    return json.loads(buf.value.decode())
+
+
+def iaat_paper_tile(mode, M, N):
+    """Paper-faithful SGEMM_NN tiling (mode 0 Alg. 2 literal, 1 optimum over Table I)."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    st = _lib.iaat_paper_tile(mode, M, N, buf, len(buf))
+    if st != 0:
+        raise IaatError(st, "iaat_paper_tile")
     return json.loads(buf.value.decode())
 
 
