@@ -239,17 +239,20 @@ def run_ours(args, rank, world, local_rank):
     A = B = C = None  # only bufs holds the operand sets (config 5 frees them chunk by chunk)
     torch.cuda.synchronize()
 
-    def call(s, lo, cnt):
+    def call(s, lo, cnt, strm=None):
+        strm = stream if strm is None else strm
         ra, ca, rb, cb = s.stored()
         A, B, C = bufs[(s.dtype, s.M, s.N, s.K, s.tr, cnt)]
         st = iaat.iaat_gemm_strided_batched(s.dt_index, s.tr[0], s.tr[1], s.M, s.N, s.K,
                                             s.alpha, A.data_ptr(), ra, ra * ca, B.data_ptr(), rb, rb * cb,
-                                            s.beta, C.data_ptr(), s.M, s.M * s.N, cnt, stream.cuda_stream)
+                                            s.beta, C.data_ptr(), s.M, s.M * s.N, cnt, strm.cuda_stream)
         if st != 0:
             raise RuntimeError("iaat call failed: %s (%s)" % (iaat.iaat_status_string(st), s.name()))
 
     if args.config == 5:
         return run_chunked_config5(args, rank, world, local_rank, shapes, desc, chunks, bufs, call)
+    if args.grouped:
+        return run_grouped(args, rank, world, local_rank, shapes, desc, chunks, bufs, stream)
 
     def step(evs=None):
         for i, (s, lo, cnt) in enumerate(chunks):
@@ -338,9 +341,94 @@ def run_ours(args, rank, world, local_rank):
                              "as workload states", "parallelism": "dp%d (batch shards, no collective)" % world},
             "roofline": roof, "gpu_launches": int(n_launch), "clocks": clk, "e2e": e2e,
             "shapes": shapes_out}
+    if args.config == 1:
+        line["hot_graph"] = run_graph_hot(chunks, call, stream)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = run_cpu_baseline(shapes, args)
     return line
+
+
+def run_graph_hot(chunks, call, stream, reps=100):
+    """Config 1 is launch/latency-bound: one 16^3 x 2000 call is
+    ~3 us of GPU work behind ~15 us of host submission.  Reported beside the
+    per-call number, labelled: the same call captured 100 times back to back
+    in a CUDA graph and replayed (operands L2-resident: 8 MB), device time per
+    call.  Not the headline value."""
+    import torch
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        for s, lo, cnt in chunks:
+            call(s, lo, cnt, torch.cuda.current_stream())  # warm the plan cache on this stream
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(reps):
+                for s, lo, cnt in chunks:
+                    call(s, lo, cnt, torch.cuda.current_stream())
+    stream.wait_stream(side)
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / reps
+    fl = sum(s.flops(cnt) for s, lo, cnt in chunks)
+    return {"us_per_call": round(us, 3), "gflops": round(fl / us / 1e3, 1), "calls": reps,
+            "label": "hot: CUDA-graph replay of %d back-to-back calls, L2-resident operands" % reps}
+
+
+def run_grouped(args, rank, world, local_rank, shapes, desc, chunks, bufs, stream):
+    """the whole workload (e.g. config 3's 64 shapes) as ONE
+    grouped call per step (iaat_gemm_grouped_strided: one plan per size
+    class, groups enqueued back to back by the library)."""
+    import torch
+    from paper_2208_09822_b200 import iaat
+    groups = []
+    for s, lo, cnt in chunks:
+        ra, ca, rb, cb = s.stored()
+        A, B, C = bufs[(s.dtype, s.M, s.N, s.K, s.tr, cnt)]
+        groups.append(dict(transA=s.tr[0], transB=s.tr[1], M=s.M, N=s.N, K=s.K, alpha=s.alpha, A=A.data_ptr(),
+                           lda=ra, strideA=ra * ca, B=B.data_ptr(), ldb=rb, strideB=rb * cb, beta=s.beta,
+                           C=C.data_ptr(), ldc=s.M, strideC=s.M * s.N, batch=cnt))
+    dt = shapes[0].dt_index
+
+    def step():
+        st = iaat.iaat_gemm_grouped_strided(dt, groups, stream.cuda_stream)
+        if st != 0:
+            raise RuntimeError("grouped call failed: %s" % iaat.iaat_status_string(st))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local_rank)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    n0 = iaat.iaat_launch_count()
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    n_launch = iaat.iaat_launch_count() - n0
+    clk = clocks.stop()
+    ms = allreduce_max(t0.elapsed_time(t1), world) / args.steps
+    flops = sum(s.flops(cnt) for s, lo, cnt in chunks)
+    byts = sum(s.alg_bytes(cnt) for s, lo, cnt in chunks)
+    pk = peaks()
+    return {"metric": METRIC, "value": round(flops * world / (ms * 1e-3) / 1e9, 1), "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": shapes[0].dtype,
+            "data": "synthetic",
+            "config": {"workload": desc + " -- as ONE grouped call per step (SURVEY f4)", "groups": len(groups)},
+            "roofline": {"bound": "hbm", "achieved": round(byts / (ms * 1e-3) / 1e9, 1), "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": round(byts / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], 4),
+                         "traffic": None, "kernel": "whole grouped call (all %d groups)" % len(groups)},
+            "gpu_launches": int(n_launch), "clocks": clk}
 
 
 def run_chunked_config5(args, rank, world, local_rank, shapes, desc, chunks, bufs, call):
@@ -575,6 +663,8 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--grouped", action="store_true",
+                    help="run the workload as one grouped (variable-size) call per step (SURVEY f4)")
     args = ap.parse_args(argv)
     rank, world, local = init_dist()
     if args.impl == "reference":

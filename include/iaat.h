@@ -97,6 +97,21 @@ iaat_status_t iaat_gemm_batched(
     const void *beta, void *const *Carray, int64_t ldc,
     int64_t batch, void *stream);
 
+/* Grouped (variable-size) strided batches: group g is one
+ * strided batched call with its own transA[g], transB[g], M[g], N[g], K[g],
+ * alpha/beta (entry g of HOST arrays of scalars of the dtype; complex: (re,
+ * im) pairs), DEVICE base pointers A[g], B[g], C[g] (held in HOST arrays),
+ * ld's, strides and batch[g].  Each group is planned for its own size class
+ * and enqueued in order on `stream`; every group is validated first, so on
+ * any argument error nothing is enqueued.                                  */
+iaat_status_t iaat_gemm_grouped_strided(
+    iaat_dtype_t dtype, int64_t group_count, const char *transA, const char *transB,
+    const int64_t *M, const int64_t *N, const int64_t *K, const void *alpha,
+    const void *const *A, const int64_t *lda, const int64_t *strideA,
+    const void *const *B, const int64_t *ldb, const int64_t *strideB,
+    const void *beta, void *const *C, const int64_t *ldc, const int64_t *strideC,
+    const int64_t *batch, void *stream);
+
 /* Typed convenience wrappers (scalars by value). */
 iaat_status_t iaat_sgemm_strided_batched(char transA, char transB, int64_t M, int64_t N,
     int64_t K, float alpha, const float *A, int64_t lda, int64_t strideA, const float *B,

@@ -489,6 +489,42 @@ iaat_status_t iaat_catalog_describe(char *json, size_t cap)
     return IAAT_SUCCESS;
 }
 
+iaat_status_t iaat_gemm_grouped_strided(iaat_dtype_t dtype, int64_t group_count, const char *transA,
+                                        const char *transB, const int64_t *M, const int64_t *N, const int64_t *K,
+                                        const void *alpha, const void *const *A, const int64_t *lda,
+                                        const int64_t *strideA, const void *const *B, const int64_t *ldb,
+                                        const int64_t *strideB, const void *beta, void *const *C, const int64_t *ldc,
+                                        const int64_t *strideC, const int64_t *batch, void *stream)
+{
+    // variable-size batches -- one plan per size class (group),
+    // every group validated before anything is enqueued.
+    if (group_count < 0) return IAAT_ERROR_INVALID_VALUE;
+    if (group_count == 0) return IAAT_SUCCESS;
+    if (!transA || !transB || !M || !N || !K || !alpha || !A || !lda || !strideA || !B || !ldb || !strideB ||
+        !beta || !C || !ldc || !strideC || !batch)
+        return IAAT_ERROR_INVALID_VALUE;
+    const int es = elt_bytes(dtype) / ((dtype == IAAT_C32F || dtype == IAAT_C64F) ? 2 : 1);  // scalar bytes
+    const int ns = (dtype == IAAT_C32F || dtype == IAAT_C64F) ? 2 : 1;                       // scalars per alpha
+    const char *al = static_cast<const char *>(alpha), *be = static_cast<const char *>(beta);
+    for (int64_t g = 0; g < group_count; ++g) {
+        const int ta = parse_op(transA[g]), tb = parse_op(transB[g]);
+        iaat_status_t st = validate(dtype, ta, tb, M[g], N[g], K[g], lda[g], ldb[g], ldc[g], batch[g],
+                                    al + g * ns * es, be + g * ns * es);
+        if (st != IAAT_SUCCESS) return st;
+        if (strideA[g] < 0 || strideB[g] < 0 || strideC[g] < 0) return IAAT_ERROR_INVALID_VALUE;
+        if (batch[g] > 1 && M[g] > 0 && N[g] > 0 && strideC[g] < (N[g] - 1) * ldc[g] + M[g])
+            return IAAT_ERROR_INVALID_VALUE;
+        if (M[g] > 0 && N[g] > 0 && batch[g] > 0 && !C[g]) return IAAT_ERROR_INVALID_VALUE;
+    }
+    for (int64_t g = 0; g < group_count; ++g) {
+        iaat_status_t st = run(dtype, transA[g], transB[g], M[g], N[g], K[g], al + g * ns * es, A[g], lda[g],
+                               strideA[g], B[g], ldb[g], strideB[g], be + g * ns * es, C[g], ldc[g], strideC[g],
+                               batch[g], nullptr, nullptr, nullptr, false, stream);
+        if (st != IAAT_SUCCESS) return st;  // only device-side (CUDA) errors can remain here
+    }
+    return IAAT_SUCCESS;
+}
+
 iaat_status_t iaat_paper_tile(int mode, int64_t M, int64_t N, char *json, size_t cap)
 {
     if ((mode != 0 && mode != 1) || M < 1 || N < 1 || M > 4096 || N > 4096 || !json) return IAAT_ERROR_INVALID_VALUE;

@@ -30,7 +30,7 @@ EXPORTS = [
     "iaat_gemm_strided_batched", "iaat_gemm_batched",
     "iaat_sgemm_strided_batched", "iaat_dgemm_strided_batched",
     "iaat_sgemm_batched", "iaat_dgemm_batched",
-    "iaat_cgemm_strided_batched", "iaat_zgemm_strided_batched",
+    "iaat_cgemm_strided_batched", "iaat_zgemm_strided_batched", "iaat_gemm_grouped_strided",
     "iaat_is_small_gemm", "iaat_plan_describe", "iaat_catalog_describe", "iaat_paper_tile",
     "iaat_status_string", "iaat_last_cuda_error", "iaat_launch_count", "iaat_version",
 ]
@@ -58,6 +58,11 @@ def _load():
     lib.iaat_plan_describe.argtypes = [i, c, c, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i, i,
                                        i64, i, ctypes.c_char_p, ctypes.c_size_t]
     lib.iaat_plan_describe.restype = i
+    P = ctypes.POINTER
+    lib.iaat_gemm_grouped_strided.argtypes = [i, i64, ctypes.c_char_p, ctypes.c_char_p, P(i64), P(i64), P(i64),
+                                              vp, P(vp), P(i64), P(i64), P(vp), P(i64), P(i64), vp, P(vp),
+                                              P(i64), P(i64), P(i64), vp]
+    lib.iaat_gemm_grouped_strided.restype = i
     lib.iaat_paper_tile.argtypes = [i, i64, i64, ctypes.c_char_p, ctypes.c_size_t]
     lib.iaat_paper_tile.restype = i
     lib.iaat_catalog_describe.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
@@ -118,6 +123,28 @@ def iaat_plan_describe(dtype, transA, transB, M, N, K, lda, strideA, ldb, stride
     if st != 0:
         raise IaatError(st, "iaat_plan_describe")
     return json.loads(buf.value.decode())
+
+
+def iaat_gemm_grouped_strided(dtype, groups, stream=0):
+    """groups: list of dicts with keys transA, transB, M, N, K, alpha, A, lda,
+    strideA, B, ldb, strideB, beta, C, ldc, strideC, batch (A/B/C integer
+    device addresses).  Marshals the host arrays of the C ABI; returns status."""
+    n = len(groups)
+    i64a = lambda key: (ctypes.c_int64 * max(n, 1))(*[int(g[key]) for g in groups])  # noqa: E731
+    ptra = lambda key: (ctypes.c_void_p * max(n, 1))(*[g[key] for g in groups])  # noqa: E731
+    if dtype in (IAAT_C32F, IAAT_C64F):
+        ct = ctypes.c_float if dtype == IAAT_C32F else ctypes.c_double
+        flat = lambda key: (ct * max(2 * n, 1))(*[x for g in groups for x in (complex(g[key]).real,  # noqa: E731
+                                                                                 complex(g[key]).imag)])
+    else:
+        ct = ctypes.c_float if dtype == IAAT_R32F else ctypes.c_double
+        flat = lambda key: (ct * max(n, 1))(*[float(g[key]) for g in groups])  # noqa: E731
+    ta = "".join(g["transA"] for g in groups).encode()
+    tb = "".join(g["transB"] for g in groups).encode()
+    return _lib.iaat_gemm_grouped_strided(dtype, n, ta, tb, i64a("M"), i64a("N"), i64a("K"), flat("alpha"),
+                                          ptra("A"), i64a("lda"), i64a("strideA"), ptra("B"), i64a("ldb"),
+                                          i64a("strideB"), flat("beta"), ptra("C"), i64a("ldc"), i64a("strideC"),
+                                          i64a("batch"), stream)
 
 
 def iaat_paper_tile(mode, M, N):

@@ -58,3 +58,18 @@ def test_no_gpu_call_fails_cleanly():
     st = iaat.iaat_gemm_strided_batched(0, "N", "N", 4, 4, 4, 1.0, 256, 4, 16, 512, 4, 16, 0.0, 1024, 4, 16, 2)
     assert st in (3, 4)
     assert iaat.iaat_status_string(st).startswith("IAAT_ERROR")
+
+
+def test_grouped_validation_before_any_launch():
+    """every group is validated before anything is enqueued; the
+    errors come back as statuses with no device involved (no GPU here)."""
+    from paper_2208_09822_b200 import iaat
+    g = dict(transA="N", transB="N", M=4, N=4, K=4, alpha=1.0, A=256, lda=4, strideA=16, B=512, ldb=4, strideB=16,
+             beta=0.0, C=1024, ldc=4, strideC=16, batch=2)
+    assert iaat.iaat_gemm_grouped_strided(0, []) == 0
+    assert iaat.iaat_gemm_grouped_strided(0, [g, dict(g, lda=2)]) == 1          # INVALID_VALUE (lda < M)
+    assert iaat.iaat_gemm_grouped_strided(0, [g, dict(g, transA="C")]) == 1      # INVALID_VALUE (op)
+    assert iaat.iaat_gemm_grouped_strided(0, [dict(g, M=81, N=81, K=81, lda=81, ldb=81, ldc=81,
+                                                    strideC=6561)]) == 2          # NOT_SMALL
+    assert iaat.iaat_gemm_grouped_strided(0, [dict(g, strideC=3)]) == 1          # overlapping C
+    assert iaat.iaat_gemm_grouped_strided(2, [dict(g, alpha=1j, beta=0.5 - 1j), dict(g, lda=1)]) == 1

@@ -442,3 +442,33 @@ def test_ks_dmma_fp64_parity(tr):
                         c.check(sample_ids(c.batch, 48, 24))
     finally:
         _force()
+
+
+@pytest.mark.parametrize("dtype", [F32, F64])
+def test_grouped_variable_size_batches(dtype):
+    """one grouped call over groups of different shapes,
+    transpositions, alpha/beta and batch sizes equals the oracle, and is
+    bitwise equal to the same groups called one by one."""
+    from paper_2208_09822_b200 import iaat
+    specs = [("N", "N", 7, 13, 5, 300, 1.0, 0.0), ("T", "N", 17, 3, 23, 1000, -1.0, 0.25),
+             ("N", "T", 32, 32, 32, 500, 1.5, 0.5), ("T", "T", 1, 61, 7, 77, 2.0, 1.0),
+             ("N", "N", 64, 48, 40, 200, 0.5, -0.5)]
+    cases = [Case(dtype, ta, tb, M, N, K, b, 11 + i, al, be) for i, (ta, tb, M, N, K, b, al, be) in enumerate(specs)]
+    ref_C = []
+    for c in cases:  # group by group through the strided API
+        c2 = Case(dtype, c.tA, c.tB, c.M, c.N, c.K, c.batch, c.seed, c.alpha, c.beta)
+        c2.run()
+        ref_C.append(c2)
+    groups = []
+    for c in cases:
+        A, B, C = c.views()
+        groups.append(dict(transA=c.tA, transB=c.tB, M=c.M, N=c.N, K=c.K, alpha=c.alpha, A=A.data_ptr(), lda=c.lda,
+                           strideA=c.sA, B=B.data_ptr(), ldb=c.ldb, strideB=c.sB, beta=c.beta, C=C.data_ptr(),
+                           ldc=c.ldc, strideC=c.sC, batch=c.batch))
+    st = iaat.iaat_gemm_grouped_strided(0 if dtype == F32 else 1, groups,
+                                        torch.cuda.current_stream().cuda_stream)
+    assert st == 0
+    torch.cuda.synchronize()
+    for c, r in zip(cases, ref_C):
+        c.check()
+        assert bits_equal(c.views()[2], r.views()[2])
