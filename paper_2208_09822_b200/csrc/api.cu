@@ -315,6 +315,11 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
             for (const KsdEntry &e : kLaunchKsd)
                 if (e.trans == ta * 2 + tb && 8 * e.wm == kp.cls[0].mr && 8 * e.wn == kp.cls[0].nr) fn = e.fn;
             if (!fn) return IAAT_ERROR_NOT_SUPPORTED;
+        } else if (plan.single == 2) {
+            fn = nullptr;
+            for (const KsuEntry &e : kLaunchKsu)
+                if (e.trans == ta * 2 + tb && e.mr == kp.cls[0].mr && e.nr == kp.cls[0].nr) fn = e.fn;
+            if (!fn) return IAAT_ERROR_NOT_SUPPORTED;
         } else if (plan.single) {
             fn = nullptr;
             for (const Ks1Entry &e : kLaunchKs1)

@@ -276,7 +276,11 @@ __device__ __forceinline__ void ks_chunk(ACC &acc, const unsigned char *smem, ui
 }
 
 // ------------------------------------------------------------------ FMA class (per-thread tile)
-template <typename T, bool TA, bool TB, int MR, int NR, int UNR>
+// UMODE: 0 = choose the swizzle addressing per call (uniform-phase or
+// general code path, both compiled); 1 = uniform-phase only (the planner
+// guarantees tm, tn multiples of 8 for the K-major dims); 2 = general only.
+// Single paths keep the register footprint of the big tiles down.
+template <typename T, bool TA, bool TB, int MR, int NR, int UNR, int UMODE = 0>
 __device__ __forceinline__ void ks_fma_class_loop(const IaatKsParams &p, const IaatClass &c, unsigned char *smem,
                                                   uint64_t *full, uint64_t *empty, int warp, int lane)
 {
@@ -350,7 +354,13 @@ __device__ __forceinline__ void ks_fma_class_loop(const IaatKsParams &p, const I
                 const uint32_t sa = ring_off + (uint32_t)(s * stage_bytes), sb = sa + (uint32_t)a_bytes;
                 const int kv = min(kc, K - ch * kc);
                 // warp-uniform: one code path per swizzle-phase case
-                if (ua && ub)
+                if (UMODE == 1)
+                    ks_chunk<T, AK, BK, AK, BK, MR, NR, UNR>(acc, smem, sa, sb, ra, rbB, a_mn, b_mn, a_pb, b_pb,
+                                                             a_rs, b_rs, kv);
+                else if (UMODE == 2)
+                    ks_chunk<T, AK, BK, false, false, MR, NR, UNR>(acc, smem, sa, sb, ra, rbB, a_mn, b_mn, a_pb,
+                                                                   b_pb, a_rs, b_rs, kv);
+                else if (ua && ub)
                     ks_chunk<T, AK, BK, AK, BK, MR, NR, UNR>(acc, smem, sa, sb, ra, rbB, a_mn, b_mn, a_pb, b_pb,
                                                              a_rs, b_rs, kv);
                 else if (ua)

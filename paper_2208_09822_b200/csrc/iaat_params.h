@@ -26,6 +26,7 @@ enum IaatFamily : int {
     IAAT_FAM_KS_FMA = 2,  // FMA tiles, K-streamed TMA staging (iaat_ks.cuh)
     IAAT_FAM_KS_DMMA = 3, // DMMA warp tiles, K-streamed TMA staging (fp64 only)
     IAAT_FAM_KS1_FMA = 4, // single-class K-streamed kernels (one per tile; the big tiles)
+    IAAT_FAM_KSU_FMA = 6, // single-class K-streamed fp32, uniform swizzle phase only (tm/tn % 8 == 0)
 };
 
 // One tile class: all tiles of one exact size (mr x nr) inside one row strip

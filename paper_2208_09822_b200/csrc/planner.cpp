@@ -436,7 +436,7 @@ Plan make_plan(const PlanRequest &r)
 
 Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn)
 {
-    if (kn.fam == IAAT_FAM_KS_FMA || kn.fam == IAAT_FAM_KS_DMMA) {
+    if (kn.fam == IAAT_FAM_KS_FMA || kn.fam == IAAT_FAM_KS_DMMA || kn.fam == IAAT_FAM_KSU_FMA) {
         Plan ksplan;
         if (plan_ks(r, kn, ksplan)) return ksplan;
         ksplan.status = 5;
@@ -867,14 +867,20 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
             // one class covering C -> its single-class kernel if generated;
             // otherwise every class must be in the multi-class kernel
             const bool one = ms.n == 1 && ns.n == 1;
-            const int single = one && catalog_has(r.dtype, tidx, IAAT_FAM_KS1_FMA, ms.s[0].size, ns.s[0].size) ? 1 : 0;
+            int single = one && catalog_has(r.dtype, tidx, IAAT_FAM_KS1_FMA, ms.s[0].size, ns.s[0].size) ? 1 : 0;
+            if (kn.fam == IAAT_FAM_KSU_FMA) {
+                // uniform-phase kernels: one class whose K-major tile counts are multiples of 8
+                if (!one || !catalog_has(r.dtype, tidx, IAAT_FAM_KSU_FMA, ms.s[0].size, ns.s[0].size)) continue;
+                if ((AK && ms.s[0].count % 8) || (BK && ns.s[0].count % 8)) continue;
+                single = 2;
+            }
             int64_t memops = 2 * M * N;
             int rb = 0;
             for (int a = 0; a < ms.n && avail; ++a) {
                 int cb = 0;
                 for (int b = 0; b < ns.n; ++b) {
                     const int mr = ms.s[a].size, nr = ns.s[b].size;
-                    if (!single && !catalog_has(r.dtype, tidx, IAAT_FAM_KS_FMA, mr, nr)) {
+                    if (single == 0 && !catalog_has(r.dtype, tidx, IAAT_FAM_KS_FMA, mr, nr)) {
                         avail = false;
                         break;
                     }
@@ -1150,7 +1156,7 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
         const IaatKsParams &q = p.ksp;
         add("\"family\": \"%s\", \"vec\": %d, \"P\": %d, \"S\": %d, \"compute_warps\": %d, "
             "\"ctas_per_sm\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, \"ngroups\": %lld, ",
-            p.ksd ? "ks_dmma" : p.single ? "ks1_fma" : "ks_fma", p.vec, q.P, q.S, q.n_compute_warps, p.ctas, p.grid, p.block, p.smem,
+            p.ksd ? "ks_dmma" : p.single == 2 ? "ksu_fma" : p.single ? "ks1_fma" : "ks_fma", p.vec, q.P, q.S, q.n_compute_warps, p.ctas, p.grid, p.block, p.smem,
             (long long)q.nunits);
         add("\"kc\": %d, \"nchunks\": %d, \"a_bytes\": %d, \"b_bytes\": %d, \"a_pitch\": %d, \"b_pitch\": %d, "
             "\"a_swizzle128\": %d, \"b_swizzle128\": %d, \"c_vec\": %d, ",

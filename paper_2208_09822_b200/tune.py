@@ -167,7 +167,7 @@ def tune_shape(sh, log):
             p = b.plan()
             if p["status"] != 0:
                 return None
-            if kw.get("family") in (2, 3) and not p["family"].startswith("ks"):
+            if kw.get("family") in (2, 3, 6) and not p["family"].startswith("ks"):
                 return None  # K-streamed plan not applicable: the planner fell back
             us = b.time_us()
         except Exception:
@@ -202,13 +202,19 @@ def tune_shape(sh, log):
                 for P in (1, 2, 3, 4):
                     for ctas in (1, 2, 3, 4):
                         trial(family=2, tile=tile, order=order, p=P, ctas=ctas)
+    if dtype == "f32" and tr != "TN" and max(M, N, K) >= 24:  # uniform-phase K-streamed big tiles
+        for tile in ("8x8", "8x6", "6x8", "8x4", "4x8"):
+            for order in (0, 5, 9, 17):
+                for P in (1, 2, 3, 4):
+                    for ctas in (1, 2, 3, 4):
+                        trial(family=6, tile=tile, order=order, p=P, ctas=ctas)
     if beta != 0:  # C_in from global (L2-prefetched) instead of staged: frees smem
         per_ab = (M * K + K * N) * elt
         for (mr, nr) in tile_options(M, N):
             for P in sorted({max(1, int(kb * 1024) // per_ab) for kb in (24, 48, 96)}):
                 trial(tile="%dx%d" % (mr, nr), p=P, csmem=0)
     results.sort(key=lambda x: x[0])
-    top = [r for r in results if r[1].get("family") not in (2, 3)][:4]
+    top = [r for r in results if r[1].get("family") not in (2, 3, 6)][:4]
     for us, kw, p in top:
         for order in (0, 1, 3, 5, 9, 17):
             for ctas in (1, 2, 3, 4):

@@ -53,6 +53,10 @@ def main():
             tiles = ["4x8", "8x4", "4x4", "6x8", "8x6", "5x8", "8x5", "4x6", "6x4"]
             grid = [dict(family=2, tile=t, order=o, p=P, ctas=c)
                     for t, o, P, c in itertools.product(tiles, (0, 1, 5, 9), (1, 2, 3, 4), (1, 2, 3, 4))]
+        if os.environ.get("KS_PROBE_FAM") == "6":
+            grid = [dict(family=6, tile=t, order=o, p=P, ctas=c)
+                    for t, o, P, c in itertools.product(["8x8", "8x6", "6x8", "8x4", "4x8"], (0, 1, 3, 5, 9, 17),
+                                                        (1, 2, 3, 4, 6), (1, 2, 3, 4))]
         for kw in grid:
             set_knobs(**kw)
             try:
