@@ -92,3 +92,26 @@ def test_two_rank_gloo_shards_match_unsharded():
     ref, _, _ = oracle.ref_gemm("N", "N", M, N, K, 1.5, A, M, M * K, B, K, K * N, 0.5, C, M, M * N, total)
     assert np.array_equal(sharded, ref)
     assert tmax == 2.0
+
+
+def test_bench_reference_arm_under_torchrun_world2():
+    """bench.py launched the way the driver launches N > 1 (torchrun, one
+    process per rank, 127.0.0.1 rendezvous), here on CPU with gloo: rank 0
+    alone runs the reference arm and prints exactly one JSON line; rank 1
+    exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--config", "1",
+           "--cpu-frac", "0.01"]
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=root, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
