@@ -142,9 +142,18 @@ class Bench:
         self.torch.cuda.empty_cache()
 
 
-def key_line(dt, tr, M, N, K, beta0, vec=1):
+def key_line(dt, tr, M, N, K, beta0):
+    """The planner's tuning-table key for a packed strided call with 256 B
+    aligned bases (csrc/planner.cpp make_plan): the 16-byte vector legality
+    field must be the planner's own (every ld and problem stride a multiple
+    of 16 bytes) or the entry never matches."""
     ra = M if tr[0] == "N" else K
     rb = K if tr[1] == "N" else N
+    ca = K if tr[0] == "N" else M
+    cb = N if tr[1] == "N" else K
+    elt = (4, 8, 8, 16)[dt]
+    al = lambda el: (el * elt) % 16 == 0  # noqa: E731
+    vec = int(al(ra) and al(rb) and al(M) and al(ra * ca) and al(rb * cb) and al(M * N))
     return "%d %d %d %d %d %d %d %d %d %d %d %d" % (dt, tr[0] == "T", tr[1] == "T", M, N, K, ra, rb, M, 1,
                                                      int(beta0), vec)
 
