@@ -305,7 +305,12 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
         kp.alpha = a;
         kp.beta = b;
         alignas(64) CUtensorMap tmA, tmB;
-        if (!encode_tmap(tmA, plan.tmA, A, elt) || !encode_tmap(tmB, plan.tmB, B, elt)) {
+        if (kp.ldgsts) {
+            std::memset(&tmA, 0, sizeof tmA);  // cp.async staging: no tensor maps
+            std::memset(&tmB, 0, sizeof tmB);
+            kp.A = static_cast<const char *>(A);
+            kp.B = static_cast<const char *>(B);
+        } else if (!encode_tmap(tmA, plan.tmA, A, elt) || !encode_tmap(tmB, plan.tmB, B, elt)) {
             g_last_cuda_error = (int)cudaErrorInvalidValue;
             return IAAT_ERROR_CUDA;
         }

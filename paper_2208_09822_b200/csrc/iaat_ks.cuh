@@ -63,6 +63,95 @@ __device__ __forceinline__ unsigned char *ks_ring(unsigned char *smem)
     return smem + (r - b);
 }
 
+// ------------------------------------------------------------------ LDGSTS producer
+// Misaligned inputs (odd ld, element-aligned bases): the whole producer warp
+// copies each chunk element by element with cp.async (4 or 8 bytes, any
+// element alignment) from the caller's layout into the same stage layout the
+// TMA boxes produce (MN-major [P][kc][pitch] / K-major [P][D][kc] swizzled),
+// lanes walking the contiguous global dimension (coalesced).  Completion:
+// each lane's cp.async.mbarrier.arrive.noinc on full[s] (count 32).  Only
+// valid elements are copied; the compute warps never read past them.
+__device__ __forceinline__ void cp_async_elem(void *dst, const void *src, int bytes)
+{
+    if (bytes == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_arrive(uint64_t *bar)
+{
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// One operand's chunk [k0, k0 + kv) of problem p (global index b) into its stage region.
+//   KMAJ: element (row r < D, k) lives at X[b*sX + r*ld + k]   -> swizzled [p*D + r][k - k0]
+//   else: element (row r < D, k) lives at X[b*sX + k*ld + r]   -> [p][k - k0][pitch]
+template <typename T, bool KMAJ>
+__device__ __forceinline__ void ldgsts_chunk(unsigned char *region, const char *X, int64_t sX, int ld, int D,
+                                             int pitch, int kc, int p, int64_t b, int k0, int kv, int lane)
+{
+    const T *src = reinterpret_cast<const T *>(X) + b * sX;
+    const int n = D * kv;
+    for (int e = lane; e < n; e += 32) {
+        int r, kk;
+        if (KMAJ) {
+            r = e / kv;
+            kk = e - r * kv;
+        } else {
+            kk = e / D;
+            r = e - kk * D;
+        }
+        const int k = k0 + kk;
+        const T *g = KMAJ ? src + (int64_t)r * ld + k : src + (int64_t)k * ld + r;
+        uint32_t off;
+        if (KMAJ) {
+            const int ra = p * D + r;
+            const int q = kk / (16 / (int)sizeof(T)), w = kk % (16 / (int)sizeof(T));
+            off = (((uint32_t)ra << 7) | ((uint32_t)(q ^ (ra & 7)) << 4)) + (uint32_t)w * sizeof(T);
+        } else {
+            off = (uint32_t)(((p * kc + kk) * pitch + r) * (int)sizeof(T));
+        }
+        cp_async_elem(region + off, g, (int)sizeof(T));
+    }
+}
+
+template <typename T, bool TA, bool TB>
+__device__ void ks_producer_ldgsts(const IaatKsParams &p, unsigned char *smem, uint64_t *full, uint64_t *empty,
+                                   int lane)
+{
+    constexpr bool AK = TA, BK = !TB;
+    unsigned char *ring = ks_ring(smem);
+    int s = 0, it = 0;
+    uint32_t phase = 0;
+    for (int64_t u = blockIdx.x; u < p.nunits; u += gridDim.x) {
+        const int64_t b0 = u * p.P;
+        const int np = (int)min((int64_t)p.P, p.batch - b0);
+        if (!p.beta_zero && lane == 0) {
+            const int64_t scb = p.sC * (int64_t)sizeof(T);
+            const char *first = p.C + b0 * scb;
+            const int64_t span = (int64_t)(np - 1) * scb + ((int64_t)(p.N - 1) * p.ldc + p.M) * (int64_t)sizeof(T);
+            uintptr_t lo = reinterpret_cast<uintptr_t>(first) & ~(uintptr_t)15;
+            uintptr_t hi = (reinterpret_cast<uintptr_t>(first) + (uintptr_t)span + 15) & ~(uintptr_t)15;
+            bulk_prefetch_l2(reinterpret_cast<const void *>(lo), (uint32_t)(hi - lo));
+        }
+        for (int c = 0; c < p.nchunks; ++c, ++it) {
+            if (it >= p.S) mbar_wait(&empty[s], phase);
+            unsigned char *st = ring + (size_t)s * p.stage_bytes;
+            const int k0 = c * p.kc, kv = min(p.kc, p.K - k0);
+            for (int q = 0; q < np; ++q) {
+                ldgsts_chunk<T, AK>(st, p.A, p.sA, p.lda, p.M, p.a_pitch, p.kc, q, b0 + q, k0, kv, lane);
+                ldgsts_chunk<T, BK>(st + p.a_bytes, p.B, p.sB, p.ldb, p.N, p.b_pitch, p.kc, q, b0 + q, k0, kv, lane);
+            }
+            cp_async_arrive(&full[s]);
+            if (++s == p.S) {
+                s = 0;
+                if (it >= 2 * p.S - 1) phase ^= 1u;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ producer
 // One warp, lane 0 issues.  Stage s of the ring = [A box | B box] of chunk c
 // of unit u; full[s] completes when both boxes have landed (tx bytes = the
@@ -551,14 +640,17 @@ __device__ __forceinline__ void ks_kernel_body(const CUtensorMap *tmA, const CUt
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.S; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], p.ldgsts ? 32 : 1);
             mbar_init(&empty[s], p.n_compute_warps);
         }
         fence_mbar_init();
     }
     __syncthreads();
     if (warp == p.n_compute_warps) {
-        ks_producer<T, TA, TB>(p, tmA, tmB, smem, full, empty, lane);
+        if (p.ldgsts)
+            ks_producer_ldgsts<T, TA, TB>(p, smem, full, empty, lane);
+        else
+            ks_producer<T, TA, TB>(p, tmA, tmB, smem, full, empty, lane);
         return;
     }
     if (SINGLE) {

@@ -102,6 +102,13 @@ struct IaatKsParams {
     int beta_zero;
     int c_vec;             // 16-byte C accesses legal (C base, ldc, stride aligned)
     int debug;             // measurement only (IAAT_DEBUG_KS): bit0 skip the k loop, bit1 skip the epilogue, bit2 do not wait for data (timing only)
+    // LDGSTS staging (ldgsts = 1): inputs whose ld / stride / base break the
+    // TMA 16-byte rules are copied element-wise with cp.async (any element
+    // alignment) into the SAME smem layouts the TMA boxes produce
+    int ldgsts;
+    const char *A, *B;     // base pointers (LDGSTS mode)
+    int64_t sA, sB;        // problem strides (elements)
+    int lda, ldb;
     int nclasses;
     IaatClass cls[IAAT_MAX_CLASSES];
 };

@@ -836,11 +836,15 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
     const bool AK = r.transA == 1, BK = r.transB == 0;
     const int64_t rowsA = AK ? K : M, colsA = AK ? M : K, rowsB = BK ? K : N, colsB = BK ? N : K;
     auto al16 = [&](int64_t el) { return (el * elt) % 16 == 0; };
-    if (r.align % 16 != 0 || !al16(r.lda) || !al16(r.ldb) || M > 256 || N > 256 || K < 1) return false;
-    if (r.batch > 1) {
-        if (!al16(r.sA) || !al16(r.sB) || r.sA < r.lda * colsA || r.sB < r.ldb * colsB) return false;
-        if (r.sA * elt >= (int64_t)1 << 40 || r.sB * elt >= (int64_t)1 << 40) return false;
-    }
+    if (M > 256 || N > 256 || K < 1) return false;
+    if (r.batch > 1 && (r.sA < r.lda * colsA || r.sB < r.ldb * colsB)) return false;  // (0 = broadcast: slab family)
+    // TMA boxes need 16-byte aligned bases, ld's and strides; otherwise the
+    // same stages are filled element-wise with cp.async (LDGSTS mode, FMA tiles)
+    bool tma_ok = r.align % 16 == 0 && al16(r.lda) && al16(r.ldb);
+    if (r.batch > 1 && (!al16(r.sA) || !al16(r.sB) || r.sA * elt >= (int64_t)1 << 40 || r.sB * elt >= (int64_t)1 << 40))
+        tma_ok = false;
+    const int ldgsts = tma_ok ? 0 : 1;
+    if (ldgsts && kn.fam == IAAT_FAM_KS_DMMA) return false;  // DMMA steps read the zero fill past K
     if (r.batch >= ((int64_t)1 << 31)) return false;
     const int a_pitch = AK ? kc : (int)round_up(M, vw), b_pitch = BK ? kc : (int)round_up(N, vw);
     if (a_pitch > 256 || b_pitch > 256) return false;
@@ -1092,6 +1096,11 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
     k.stage_bytes = best.a_bytes + best.b_bytes;
     k.beta_zero = r.beta_zero;
     k.c_vec = c_vec ? 1 : 0;
+    k.ldgsts = ldgsts;
+    k.sA = r.sA;
+    k.sB = r.sB;
+    k.lda = (int)r.lda;
+    k.ldb = (int)r.ldb;
     k.nclasses = best.ncls;
     for (int q = 0; q < best.ncls; ++q) k.cls[q] = best.cls[q];
     auto geo = [&](TmaGeo &g, int64_t rows, int64_t cols, int64_t ld, int64_t stride, bool kmaj, int pitch, int D) {
@@ -1159,8 +1168,9 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
             p.ksd ? "ks_dmma" : p.single == 2 ? "ksu_fma" : p.single ? "ks1_fma" : "ks_fma", p.vec, q.P, q.S, q.n_compute_warps, p.ctas, p.grid, p.block, p.smem,
             (long long)q.nunits);
         add("\"kc\": %d, \"nchunks\": %d, \"a_bytes\": %d, \"b_bytes\": %d, \"a_pitch\": %d, \"b_pitch\": %d, "
-            "\"a_swizzle128\": %d, \"b_swizzle128\": %d, \"c_vec\": %d, ",
-            q.kc, q.nchunks, q.a_bytes, q.b_bytes, q.a_pitch, q.b_pitch, p.tmA.swizzle128, p.tmB.swizzle128, q.c_vec);
+            "\"a_swizzle128\": %d, \"b_swizzle128\": %d, \"c_vec\": %d, \"ldgsts\": %d, ",
+            q.kc, q.nchunks, q.a_bytes, q.b_bytes, q.a_pitch, q.b_pitch, p.tmA.swizzle128, p.tmB.swizzle128, q.c_vec,
+            q.ldgsts);
     } else {
         add("\"family\": \"%s\", \"vec\": %d, \"P\": %d, \"S\": %d, \"compute_warps\": %d, \"ctas_per_sm\": %d, "
             "\"grid\": %d, \"block\": %d, \"smem\": %d, \"ngroups\": %lld, ",

@@ -399,17 +399,37 @@ def test_ks_family_parity_and_bitwise_vs_slab(dtype, tr):
         _force()
 
 
-def test_ks_not_applicable_falls_back():
-    """Misaligned ld (not a multiple of 16 bytes): no TMA plan exists; a
-    forced KS request falls back to the slab family and stays correct."""
+@pytest.mark.parametrize("tr", TRANS)
+@pytest.mark.parametrize("dtype", [F32, F64])
+def test_ks_ldgsts_misaligned(dtype, tr):
+    """Odd ld's / misaligned bases break the TMA 16-byte rules: the
+    K-streamed plans then fill the same stages with cp.async (LDGSTS mode).
+    Against the oracle on odd shapes (ragged chunks, ragged last unit,
+    misaligned base, padded ld with NaN), and fp32 bitwise equal to the slab
+    family."""
     from paper_2208_09822_b200 import iaat
+    shapes = [(37, 41, 43), (7, 13, 5), (29, 29, 29), (61, 11, 79), (1, 31, 67)]
     try:
-        _force(family=2)
-        c = Case(F32, "N", "N", 37, 41, 43, 200, 3, 1.0, 1.0)
-        p = iaat.iaat_plan_describe(0, "N", "N", 37, 41, 43, c.lda, c.sA, c.ldb, c.sB, c.ldc, c.sC, 200, False)
-        assert not p["family"].startswith("ks")
-        c.run()
-        c.check()
+        for (M, N, K) in shapes:
+            if tr == "TN" and M * N * K > 32768:
+                continue
+            for P, pad, off in ((1, 0, 0), (2, 1, 1)):
+                _force(family=2, p=P)
+                c = Case(dtype, tr[0], tr[1], M, N, K, 211, 17, -0.75, 1.25, pad=pad, elem_offset=off)
+                p = iaat.iaat_plan_describe(0 if dtype == F32 else 1, tr[0], tr[1], M, N, K, c.lda, c.sA, c.ldb,
+                                            c.sB, c.ldc, c.sC, c.batch, False, False, 256 if off == 0 else 4)
+                if not p["family"].startswith("ks"):
+                    continue  # e.g. P problems do not fit one CTA
+                assert p["ldgsts"] == 1, (tr, M, N, K, p)
+                c.run()
+                torch.cuda.synchronize()
+                c.check()
+                if dtype == F32:
+                    _force(family=0)
+                    c2 = Case(dtype, tr[0], tr[1], M, N, K, 211, 17, -0.75, 1.25, pad=pad, elem_offset=off)
+                    c2.run()
+                    torch.cuda.synchronize()
+                    assert bits_equal(c.views()[2], c2.views()[2]), (tr, M, N, K)
     finally:
         _force()
 
