@@ -86,33 +86,31 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t *bar)
 
 // One operand's chunk [k0, k0 + kv) of problem p (global index b) into its stage region.
 //   KMAJ: element (row r < D, k) lives at X[b*sX + r*ld + k]   -> swizzled [p*D + r][k - k0]
+//         lanes walk k (one row per warp instruction: coalesced, no division)
 //   else: element (row r < D, k) lives at X[b*sX + k*ld + r]   -> [p][k - k0][pitch]
+//         lanes walk r along each column
 template <typename T, bool KMAJ>
 __device__ __forceinline__ void ldgsts_chunk(unsigned char *region, const char *X, int64_t sX, int ld, int D,
                                              int pitch, int kc, int p, int64_t b, int k0, int kv, int lane)
 {
+    constexpr int KU = 16 / (int)sizeof(T);
     const T *src = reinterpret_cast<const T *>(X) + b * sX;
-    const int n = D * kv;
-    for (int e = lane; e < n; e += 32) {
-        int r, kk;
-        if (KMAJ) {
-            r = e / kv;
-            kk = e - r * kv;
-        } else {
-            kk = e / D;
-            r = e - kk * D;
+    if (KMAJ) {
+        if (lane < kv) {
+            const uint32_t q = (uint32_t)(lane / KU), w = (uint32_t)(lane % KU) * sizeof(T);
+            const T *g = src + k0 + lane;
+            for (int r = 0; r < D; ++r, g += ld) {
+                const int ra = p * D + r;
+                const uint32_t off = (((uint32_t)ra << 7) | ((q ^ (uint32_t)(ra & 7)) << 4)) + w;
+                cp_async_elem(region + off, g, (int)sizeof(T));
+            }
         }
-        const int k = k0 + kk;
-        const T *g = KMAJ ? src + (int64_t)r * ld + k : src + (int64_t)k * ld + r;
-        uint32_t off;
-        if (KMAJ) {
-            const int ra = p * D + r;
-            const int q = kk / (16 / (int)sizeof(T)), w = kk % (16 / (int)sizeof(T));
-            off = (((uint32_t)ra << 7) | ((uint32_t)(q ^ (ra & 7)) << 4)) + (uint32_t)w * sizeof(T);
-        } else {
-            off = (uint32_t)(((p * kc + kk) * pitch + r) * (int)sizeof(T));
+    } else {
+        for (int kk = 0; kk < kv; ++kk) {
+            const T *g = src + (int64_t)(k0 + kk) * ld;
+            unsigned char *d = region + (uint32_t)((p * kc + kk) * pitch) * sizeof(T);
+            for (int r = lane; r < D; r += 32) cp_async_elem(d + r * sizeof(T), g + r, (int)sizeof(T));
         }
-        cp_async_elem(region + off, g, (int)sizeof(T));
     }
 }
 
