@@ -88,14 +88,69 @@ struct CTile<double, MR, NR> {
 
 // acc(i,j) += sum_k opA(row0+i, k) * opB(k, col0+j), k ascending.
 //   opA(i,k) = A[i + k*lda] (N) or A[k + i*lda] (T); opB(k,j) = B[k + j*ldb] (N) or B[j + k*ldb] (T)
-template <typename R, bool TA, bool TB, int MR, int NR>
+// VEC (complex fp32 only, every address 16-byte aligned): two complex per
+// 16-byte load -- two rows (tile-contiguous operand) or two k-steps
+// (k-contiguous operand) -- in k-blocks of 2.
+template <typename R, bool TA, bool TB, int MR, int NR, bool VEC>
 __device__ __forceinline__ void cfma_tile(CTile<R, MR, NR> &acc, const typename CplxOf<R>::type *__restrict__ sA,
                                           const typename CplxOf<R>::type *__restrict__ sB, int lda, int ldb, int K,
                                           int row0, int col0)
 {
     typedef typename CplxOf<R>::type CT;
+    int k = 0;
+    if (VEC && sizeof(CT) == 8) {
+        // A tile-contiguous iff !TA; B tile-contiguous iff TB
+        constexpr bool AV = !TA && (MR % 2 == 0), BV = TB && (NR % 2 == 0);
+#pragma unroll 2
+        for (; k + 2 <= K; k += 2) {
+            CT a[2][MR], b[2][NR];
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+                if (AV) {
+#pragma unroll
+                    for (int i = 0; i < MR; i += 2) {
+                        const float4 v = *reinterpret_cast<const float4 *>(sA + row0 + i + (k + kk) * lda);
+                        a[kk][i] = CT{v.x, v.y};
+                        a[kk][i + 1] = CT{v.z, v.w};
+                    }
+                } else if (!TA) {
+#pragma unroll
+                    for (int i = 0; i < MR; ++i) a[kk][i] = sA[row0 + i + (k + kk) * lda];
+                }
+                if (BV) {
+#pragma unroll
+                    for (int j = 0; j < NR; j += 2) {
+                        const float4 v = *reinterpret_cast<const float4 *>(sB + col0 + j + (k + kk) * ldb);
+                        b[kk][j] = CT{v.x, v.y};
+                        b[kk][j + 1] = CT{v.z, v.w};
+                    }
+                } else if (TB) {
+#pragma unroll
+                    for (int j = 0; j < NR; ++j) b[kk][j] = sB[col0 + j + (k + kk) * ldb];
+                }
+            }
+            if (TA) {  // k-contiguous: (k, k+1) of each row in one 16-byte load
+#pragma unroll
+                for (int i = 0; i < MR; ++i) {
+                    const float4 v = *reinterpret_cast<const float4 *>(sA + k + (row0 + i) * lda);
+                    a[0][i] = CT{v.x, v.y};
+                    a[1][i] = CT{v.z, v.w};
+                }
+            }
+            if (!TB) {
+#pragma unroll
+                for (int j = 0; j < NR; ++j) {
+                    const float4 v = *reinterpret_cast<const float4 *>(sB + k + (col0 + j) * ldb);
+                    b[0][j] = CT{v.x, v.y};
+                    b[1][j] = CT{v.z, v.w};
+                }
+            }
+            acc.mac(a[0], b[0]);
+            acc.mac(a[1], b[1]);
+        }
+    }
 #pragma unroll 4
-    for (int k = 0; k < K; ++k) {
+    for (; k < K; ++k) {
         CT a[MR], b[NR];
 #pragma unroll
         for (int i = 0; i < MR; ++i) a[i] = TA ? sA[k + (row0 + i) * lda] : sA[row0 + i + k * lda];
@@ -148,7 +203,7 @@ __device__ __forceinline__ void cepilogue(const CTile<R, MR, NR> &acc, typename 
 
 // One compute warp running complex tile class `c` over all groups of this CTA
 // (the complex counterpart of fma_class_loop, same mapping and pipeline).
-template <typename R, bool TA, bool TB, int MR, int NR>
+template <typename R, bool TA, bool TB, int MR, int NR, bool VEC = false>
 __device__ __forceinline__ void cfma_class_loop(const IaatKParams &p, const IaatClass &c, unsigned char *smem,
                                                 uint64_t *full, uint64_t *empty, int warp, int lane)
 {
@@ -192,7 +247,7 @@ __device__ __forceinline__ void cfma_class_loop(const IaatKParams &p, const Iaat
             const char *b_prob = p.modeB == IAAT_STAGE_SLAB ? b_first : prob_ptr(p.B, p.Barr, sbb, b0 + pl);
             const CT *sA = reinterpret_cast<const CT *>(sv.a + smem_offset(p.modeA, a_first, a_prob, sab, p.slotA, pl));
             const CT *sB = reinterpret_cast<const CT *>(sv.b + smem_offset(p.modeB, b_first, b_prob, sbb, p.slotB, pl));
-            cfma_tile<R, TA, TB, MR, NR>(acc, sA, sB, p.lda, p.ldb, p.K, row0, col0);
+            cfma_tile<R, TA, TB, MR, NR, VEC>(acc, sA, sB, p.lda, p.ldb, p.K, row0, col0);
         }
         if (!p.c_in_smem) {
             __syncwarp();
