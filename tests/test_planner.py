@@ -180,3 +180,81 @@ def test_not_small_and_invalid():
         plan(0, "NN", 81, 81, 81)
     with pytest.raises(iaat.IaatError):
         plan(0, "TN", 33, 33, 33)
+
+
+def _forced(**kw):
+    import os
+    keys = ("IAAT_FORCE_FAMILY", "IAAT_FORCE_TILE", "IAAT_FORCE_P", "IAAT_FORCE_CTAS", "IAAT_FORCE_ORDER")
+    for k in keys:
+        os.environ.pop(k, None)
+    for k, v in kw.items():
+        os.environ["IAAT_FORCE_" + k.upper()] = str(v)
+
+
+def ks_cover(p, M, N):
+    """Exact cover under the K-streamed element maps: MN-major dims tile
+    contiguously, K-major dims interleave (row = base + t + tiles*i)."""
+    tr = p["trans"]
+    ak, bk = tr[0] == "T", tr[1] == "N"
+    cover = np.zeros((M, N), dtype=np.int32)
+    for c in p["classes"]:
+        tm, tn = c["tm"], c["tiles"] // c["tm"]
+        for ti, tj in itertools.product(range(tm), range(tn)):
+            rows = [c["row_base"] + (ti + tm * i if ak else ti * c["mr"] + i) for i in range(c["mr"])]
+            cols = [c["col_base"] + (tj + tn * j if bk else tj * c["nr"] + j) for j in range(c["nr"])]
+            for r in rows:
+                for q in cols:
+                    cover[r, q] += 1
+    return np.all(cover == 1)
+
+
+@pytest.mark.parametrize("fam", [2, 6])
+def test_forced_k_streamed_plans_are_valid(fam):
+    """K-streamed plans (families 2 = KS/KS1, 6 = uniform-phase) over a grid
+    of shapes: exact cover with their element maps, catalog membership,
+    <= 16 resident warps per SM, smem within the opt-in limit, 1024-aligned
+    stage regions, and the uniform-phase precondition."""
+    try:
+        for tr in TRANS:
+            for (M, N, K) in ((64, 64, 64), (80, 72, 48), (36, 44, 52), (16, 24, 33), (48, 48, 48), (8, 40, 16)):
+                if tr == "TN" and M * N * K > 32768:
+                    continue
+                for P in (1, 2, 3):
+                    _forced(family=fam, p=P)
+                    p = plan(0, tr, M, N, K, batch=5000)
+                    if not p["family"].startswith("ks"):
+                        continue  # not applicable: falls back to the slab planner
+                    assert ks_cover(p, M, N), (tr, M, N, K, P, p["classes"])
+                    fam_name = p["family"]
+                    for c in p["classes"]:
+                        assert (fam_name if fam_name != "ks_fma" else "ks_fma", "f32", tr, c["mr"], c["nr"]) in CATSET
+                    assert p["ctas_per_sm"] * (p["compute_warps"] + 1) <= 16
+                    assert p["smem"] * p["ctas_per_sm"] <= 228 * 1024
+                    assert p["a_bytes"] % 1024 == 0 and p["b_bytes"] % 1024 == 0
+                    assert p["block"] == 32 * (p["compute_warps"] + 1)
+                    if fam_name == "ksu_fma":
+                        c = p["classes"][0]
+                        if tr[0] == "T":
+                            assert c["tm"] % 8 == 0
+                        if tr[1] == "N":
+                            assert (c["tiles"] // c["tm"]) % 8 == 0
+    finally:
+        _forced()
+
+
+def test_fp64_default_is_k_streamed_dmma():
+    """fp64 with M, N multiples of 8 and 16-byte aligned operands plans the
+    K-streamed DMMA kernels by default; warps = P x warp tiles, one warp tile
+    each; the MN-major pitch is 4 (mod 16) doubles (conflict-free fragment
+    rows)."""
+    for tr in ("NN", "NT", "TT"):
+        for n in (16, 32, 48, 64, 80):
+            p = plan(1, tr, n, n, n, batch=200000, beta0=True)
+            assert p["family"] == "ks_dmma", (tr, n, p["family"])
+            c = p["classes"][0]
+            assert p["compute_warps"] == p["P"] * c["tiles"]
+            assert (n // c["mr"]) * (n // c["nr"]) == c["tiles"]
+            if tr[0] == "N":
+                assert p["a_pitch"] % 16 == 4
+            if tr[1] == "T":
+                assert p["b_pitch"] % 16 == 4
