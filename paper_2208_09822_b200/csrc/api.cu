@@ -301,6 +301,8 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
         IaatKsParams kp = plan.ksp;
         static const int ks_debug = std::getenv("IAAT_DEBUG_KS") ? std::atoi(std::getenv("IAAT_DEBUG_KS")) : 0;
         kp.debug = ks_debug;
+        kp.alpha_i = ai;
+        kp.beta_i = bi;
         kp.C = static_cast<char *>(C);
         kp.alpha = a;
         kp.beta = b;
@@ -310,15 +312,20 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
             std::memset(&tmB, 0, sizeof tmB);
             kp.A = static_cast<const char *>(A);
             kp.B = static_cast<const char *>(B);
-        } else if (!encode_tmap(tmA, plan.tmA, A, elt) || !encode_tmap(tmB, plan.tmB, B, elt)) {
+        } else if (!encode_tmap(tmA, plan.tmA, A, kp.cplx ? 8 : elt) || !encode_tmap(tmB, plan.tmB, B, kp.cplx ? 8 : elt)) {
             g_last_cuda_error = (int)cudaErrorInvalidValue;
             return IAAT_ERROR_CUDA;
         }
         KsLaunchFn fn = kLaunchKs[r.dtype][ta * 2 + tb];
         if (plan.ksd) {
             fn = nullptr;
-            for (const KsdEntry &e : kLaunchKsd)
-                if (e.trans == ta * 2 + tb && 8 * e.wm == kp.cls[0].mr && 8 * e.wn == kp.cls[0].nr) fn = e.fn;
+            if (kp.cplx) {
+                for (const KsdEntry &e : kLaunchKsz)
+                    if (e.trans == ta * 2 + tb && 8 * e.wm == kp.cls[0].mr && 8 * e.wn == kp.cls[0].nr) fn = e.fn;
+            } else {
+                for (const KsdEntry &e : kLaunchKsd)
+                    if (e.trans == ta * 2 + tb && 8 * e.wm == kp.cls[0].mr && 8 * e.wn == kp.cls[0].nr) fn = e.fn;
+            }
             if (!fn) return IAAT_ERROR_NOT_SUPPORTED;
         } else if (plan.single == 2) {
             fn = nullptr;

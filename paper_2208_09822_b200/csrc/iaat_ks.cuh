@@ -172,9 +172,9 @@ __device__ void ks_producer(const IaatKsParams &p, const CUtensorMap *tmA, const
         if (!p.beta_zero) {
             // C_in of the unit's problems is read by the epilogue: warm L2 now
             const int np = (int)min((int64_t)p.P, p.batch - b0);
-            const int64_t scb = p.sC * (int64_t)sizeof(T);
+            const int64_t scb = p.sC * (int64_t)p.c_elt;
             const char *first = p.C + (int64_t)b0 * scb;
-            const int64_t span = (int64_t)(np - 1) * scb + ((int64_t)(p.N - 1) * p.ldc + p.M) * (int64_t)sizeof(T);
+            const int64_t span = (int64_t)(np - 1) * scb + ((int64_t)(p.N - 1) * p.ldc + p.M) * (int64_t)p.c_elt;
             uintptr_t lo = reinterpret_cast<uintptr_t>(first) & ~(uintptr_t)15;
             uintptr_t hi = (reinterpret_cast<uintptr_t>(first) + (uintptr_t)span + 15) & ~(uintptr_t)15;
             bulk_prefetch_l2(reinterpret_cast<const void *>(lo), (uint32_t)(hi - lo));
@@ -185,10 +185,11 @@ __device__ void ks_producer(const IaatKsParams &p, const CUtensorMap *tmA, const
             unsigned char *st = ring + (size_t)s * p.stage_bytes;
             mbar_arrive_expect_tx(&full[s], tx);
             const int k0 = c * p.kc;
-            if (TA) tma_load_3d(st, tmA, k0, 0, b0, &full[s], pol);                 // A: K x M, K-major
+            const int kr = p.cplx ? 2 * k0 : k0;  // complex: K-major boxes index the real (re, im) view
+            if (TA) tma_load_3d(st, tmA, kr, 0, b0, &full[s], pol);                 // A: K x M, K-major
             else    tma_load_3d(st, tmA, 0, k0, b0, &full[s], pol);                 // A: M x K, MN-major
             if (TB) tma_load_3d(st + p.a_bytes, tmB, 0, k0, b0, &full[s], pol);     // B: N x K, MN-major
-            else    tma_load_3d(st + p.a_bytes, tmB, k0, 0, b0, &full[s], pol);     // B: K x N, K-major
+            else    tma_load_3d(st + p.a_bytes, tmB, kr, 0, b0, &full[s], pol);     // B: K x N, K-major
             if (++s == p.S) {
                 s = 0;
                 if (it >= 2 * p.S - 1) phase ^= 1u;  // lap L >= 1 waits for parity (L - 1) & 1
@@ -620,6 +621,134 @@ __device__ __forceinline__ void ks_dmma_class_loop(const IaatKsParams &p, const 
                     }
                 }
             }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ complex DMMA (ZGEMM) warp tile
+// ZGEMM on the fp64 tensor cores (SURVEY f1 + the DMMA path): TMA boxes over
+// the real view of the interleaved data (an M x K complex matrix = a 2M x K
+// real one), kc = 8 complex k-steps per chunk (K-major rows: 8 complex = 128
+// bytes, swizzled; MN-major rows: pitch >= 2M doubles, pitch = 8 mod 16).  One
+// 16-byte load gives a lane the (re, im) pair of its fragment element; four
+// DMMA per 8x8x4 complex block:
+//   D'_re += B_re^T A_re^T + (-B_im)^T A_im^T,   D'_im += B_im^T A_re^T + B_re^T A_im^T
+// (transposed form of iaat_dmma.cuh: a lane's accumulators are two
+// consecutive C rows).  k mapping: DMMA step s (2 per chunk) gives position t
+// the k-value 2t + s for both operands -- on the swizzled K-major rows the
+// 4 rows of a half-warp then touch two disjoint bank sets.  A ragged last
+// chunk reads the copy engine's zero fill past K.
+template <bool KMAJ>
+__device__ __forceinline__ uint32_t ksz_off(int r_abs, int k, int pitch_r, int pk)
+{
+    if (KMAJ) return ((uint32_t)r_abs << 7) | ((uint32_t)(k ^ (r_abs & 7)) << 4);
+    return (uint32_t)((pk + k) * pitch_r + 2 * r_abs) * 8u;
+}
+
+template <bool TA, bool TB, int WM, int WN>
+__device__ __forceinline__ void ks_zdmma_class_loop(const IaatKsParams &p, const IaatClass &c, unsigned char *smem,
+                                                    uint64_t *full, uint64_t *empty, int warp, int lane)
+{
+    constexpr bool AK = TA, BK = !TB;
+    const int K = p.K, kc = p.kc, nchunks = p.nchunks, P = p.P, S = p.S, M = p.M, N = p.N, ldc = p.ldc;
+    const int stage_bytes = p.stage_bytes, a_bytes = p.a_bytes;
+    const bool beta_zero = p.beta_zero != 0;
+    const int64_t nunits = p.nunits, batch = p.batch;
+    const int g = lane >> 2, t = lane & 3;
+    const int wi = warp - c.warp_begin;
+    const int pl = wi / c.tiles, tt = wi - pl * c.tiles;
+    const int ti = c.colfast ? tt / c.tn : tt % c.tm;
+    const int tj = c.colfast ? tt % c.tn : tt / c.tm;
+    const int row0 = c.row_base + ti * 8 * WM, col0 = c.col_base + tj * 8 * WN;
+    const int pc = min(pl, P - 1);
+    uint32_t oa[2][WM], ob[2][WN];  // [step s][block]: element k = 2t + s
+#pragma unroll
+    for (int st = 0; st < 2; ++st) {
+#pragma unroll
+        for (int mi = 0; mi < WM; ++mi)
+            oa[st][mi] = AK ? ksz_off<true>(pc * M + row0 + 8 * mi + g, 2 * t + st, 0, 0)
+                            : ksz_off<false>(row0 + 8 * mi + g, 2 * t + st, p.a_pitch, pc * kc);
+#pragma unroll
+        for (int nj = 0; nj < WN; ++nj)
+            ob[st][nj] = BK ? ksz_off<true>(pc * N + col0 + 8 * nj + g, 2 * t + st, 0, 0)
+                            : ksz_off<false>(col0 + 8 * nj + g, 2 * t + st, p.b_pitch, pc * kc);
+    }
+    const double ar = p.alpha, ai = p.alpha_i, br = p.beta, bi = p.beta_i;
+    const int64_t scb = p.sC * 16;
+    const uint32_t ring_off = (uint32_t)(ks_ring(smem) - smem);
+    const bool tile_ok = pl < P;
+
+    int s = 0;
+    uint32_t phase = 0;
+    for (int64_t u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int64_t b0 = u * P;
+        const bool active = tile_ok && (b0 + pl) < batch;
+        double re[WM][WN][2], im[WM][WN][2];
+#pragma unroll
+        for (int mi = 0; mi < WM; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < WN; ++nj) re[mi][nj][0] = re[mi][nj][1] = im[mi][nj][0] = im[mi][nj][1] = 0.0;
+        for (int ch = 0; ch < nchunks; ++ch) {
+            mbar_wait(&full[s], phase);
+            if (active) {
+                const unsigned char *sa = smem + ring_off + (uint32_t)(s * stage_bytes);
+                const unsigned char *sb = sa + a_bytes;
+                const int kv = min(kc, K - ch * kc);
+                const int nst = kv > 1 ? 2 : 1;  // step s covers k = 2t + s: all of kv when s < 2 and t < 4
+#pragma unroll 2
+                for (int st = 0; st < nst; ++st) {
+                    double2 af[WM], bf[WN];
+#pragma unroll
+                    for (int mi = 0; mi < WM; ++mi) af[mi] = *reinterpret_cast<const double2 *>(sa + oa[st][mi]);
+#pragma unroll
+                    for (int nj = 0; nj < WN; ++nj) bf[nj] = *reinterpret_cast<const double2 *>(sb + ob[st][nj]);
+#pragma unroll
+                    for (int nj = 0; nj < WN; ++nj) {
+                        const double nbi = -bf[nj].y;
+#pragma unroll
+                        for (int mi = 0; mi < WM; ++mi) {
+                            ks_dmma_8x8x4(re[mi][nj][0], re[mi][nj][1], bf[nj].x, af[mi].x);
+                            ks_dmma_8x8x4(re[mi][nj][0], re[mi][nj][1], nbi, af[mi].y);
+                            ks_dmma_8x8x4(im[mi][nj][0], im[mi][nj][1], bf[nj].y, af[mi].x);
+                            ks_dmma_8x8x4(im[mi][nj][0], im[mi][nj][1], bf[nj].x, af[mi].y);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == S) {
+                s = 0;
+                phase ^= 1u;
+            }
+        }
+        if (active) {
+            double *C = reinterpret_cast<double *>(p.C + (b0 + pl) * scb);
+            // per 8x8 block: its two C_in loads before its two stores (few live registers)
+#pragma unroll
+            for (int mi = 0; mi < WM; ++mi)
+#pragma unroll
+                for (int nj = 0; nj < WN; ++nj) {
+                    double2 ci[2];
+                    double *q0 = C + 2 * ((row0 + 8 * mi + 2 * t) + (int64_t)(col0 + 8 * nj + g) * ldc);
+                    if (!beta_zero) {
+                        ci[0] = __ldcs(reinterpret_cast<const double2 *>(q0));
+                        ci[1] = __ldcs(reinterpret_cast<const double2 *>(q0 + 2));
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const double sr = re[mi][nj][h], si = im[mi][nj][h];
+                        double tr = 0.0, tim = 0.0;
+                        if (!beta_zero) {
+                            tr = fma_rn(br, ci[h].x, mul_rn(-bi, ci[h].y));
+                            tim = fma_rn(br, ci[h].y, mul_rn(bi, ci[h].x));
+                        }
+                        double2 o;
+                        o.x = fma_rn(ar, sr, fma_rn(-ai, si, tr));
+                        o.y = fma_rn(ar, si, fma_rn(ai, sr, tim));
+                        __stcs(reinterpret_cast<double2 *>(q0 + 2 * h), o);
+                    }
+                }
         }
     }
 }

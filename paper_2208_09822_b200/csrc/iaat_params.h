@@ -106,6 +106,9 @@ struct IaatKsParams {
     // TMA 16-byte rules are copied element-wise with cp.async (any element
     // alignment) into the SAME smem layouts the TMA boxes produce
     int ldgsts;
+    int cplx;              // 1: complex fp64 (ZGEMM) DMMA kernels -- TMA boxes over the real (re, im) view
+    int c_elt;             // bytes per C element (sizeof(T), or 16 for complex fp64)
+    double alpha_i, beta_i;
     const char *A, *B;     // base pointers (LDGSTS mode)
     int64_t sA, sB;        // problem strides (elements)
     int lda, ldb;

@@ -419,7 +419,7 @@ Plan make_plan(const PlanRequest &r)
             tuned = true;
         }
     }
-    if (!kn.any() && r.dtype == 1 && r.M % 8 == 0 && r.N % 8 == 0) {
+    if (!kn.any() && (r.dtype == 1 || r.dtype == 3) && r.M % 8 == 0 && r.N % 8 == 0) {
         // fp64 on tensor cores: the K-streamed DMMA family is the default
         // wherever its TMA preconditions hold (measured 1.3-2.5x the slab
         // DMMA kernels on B200, profiles/)
@@ -826,9 +826,153 @@ void ks_class_cost(const PlanRequest &r, int elt, int mr, int nr, const Lanes &L
 
 }  // namespace
 
+// ---------------------------------------------------------------- complex fp64 on DMMA (ZGEMM)
+// K-streamed TMA boxes over the real view of the interleaved data (an R x C
+// complex matrix = a 2R x C real one, ld doubled), kc = 8 complex k-steps per
+// chunk: K-major rows of 8 complex = 128 bytes (swizzled), MN-major rows of
+// pitch >= 2D doubles with pitch = 8 (mod 16).  One warp tile per warp.
+bool plan_ks_zdmma(const PlanRequest &r, const Knobs &kn, Plan &out)
+{
+    if (!(kn.fam == IAAT_FAM_KS_DMMA || !kn.any())) return false;
+    const int64_t M = r.M, N = r.N, K = r.K;
+    if (M % 8 || N % 8 || K < 1 || M > 120 || N > 120) return false;
+    const bool AK = r.transA == 1, BK = r.transB == 0;
+    const int tidx = r.transA * 2 + r.transB;
+    const int64_t colsA = AK ? M : K, colsB = BK ? N : K, rowsA = AK ? K : M, rowsB = BK ? K : N;
+    if (r.align % 16 != 0) return false;
+    if (r.batch > 1 && (r.sA < r.lda * colsA || r.sB < r.ldb * colsB)) return false;
+    if (r.batch >= ((int64_t)1 << 31) || r.sA * 16 >= (int64_t)1 << 40 || r.sB * 16 >= (int64_t)1 << 40) return false;
+    const int kc = 8, nchunks = (int)((K + kc - 1) / kc);
+    auto zpitch = [](int64_t D) { int64_t q = 2 * D; while (q % 16 != 8) ++q; return (int)q; };
+    const int da = AK ? 16 : zpitch(M), db = BK ? 16 : zpitch(N);
+    const double hbm_per_problem = (double)(M * K + K * N + M * N * (r.beta_zero ? 1 : 2)) * 16;
+    KsCand best;
+    for (int wm = 1; wm <= 5; ++wm)
+        for (int wn = 1; wn <= 5; ++wn) {
+            if ((M / 8) % wm || (N / 8) % wn) continue;
+            if (kn.mr && (8 * wm != kn.mr || 8 * wn != kn.nr)) continue;
+            if (!catalog_has(3, tidx, IAAT_FAM_KS_DMMA, 8 * wm, 8 * wn)) continue;
+            const int tm = (int)(M / (8 * wm)), tn = (int)(N / (8 * wn)), tiles = tm * tn;
+            for (int ctas = 1; ctas <= 3; ++ctas) {
+                if (kn.ctas && ctas != kn.ctas) continue;
+                const int wmax = std::min(IAAT_MAX_THREADS / 32, 16 / ctas) - 1;
+                const int smem_cta = (int)std::min<int64_t>(IAAT_SMEM_LIMIT, 228 * 1024 / ctas - 1024);
+                for (int P = 1; P * tiles <= wmax; ++P) {
+                    if (kn.p && P != kn.p) continue;
+                    if (P > 1 && (int64_t)(P - 1) * r.sm_count * ctas >= r.batch) break;
+                    const int W = P * tiles;
+                    const int a_bytes = (int)round_up((int64_t)P * (AK ? M * 128 : (int64_t)kc * da * 8), 1024);
+                    const int b_bytes = (int)round_up((int64_t)P * (BK ? N * 128 : (int64_t)kc * db * 8), 1024);
+                    int S = std::min(IAAT_KS_MAX_STAGES, (smem_cta - IAAT_KS_BAR_BYTES - 1024) / (a_bytes + b_bytes));
+                    if (kn.s > 0) S = std::min(S, kn.s);
+                    if (S < 2) continue;
+                    const double t_hbm = ctas * P * hbm_per_problem / kHbmBytesPerClk;
+                    const double t_dmma = ctas * 4.0 * P * M * N * K / kDfmaPerClk;  // 4 real products
+                    const double t_lat = kLoadLatency * nchunks / std::max(1, S - 1) / ctas;
+                    const double t = std::max(std::max(t_hbm, t_dmma), t_lat) + 0.15 * std::min(t_hbm, t_dmma) + 300.0;
+                    const int64_t nunits = (r.batch + P - 1) / P;
+                    const int64_t slots = (int64_t)r.sm_count * ctas;
+                    const double total = t * (double)((nunits + slots - 1) / slots) + 3000.0;
+                    if (!(total < best.total * 0.995)) continue;
+                    KsCand c;
+                    c.ok = true;
+                    c.dmma = 1;
+                    c.single = 1;
+                    c.total = total;
+                    c.unit = t;
+                    c.P = P;
+                    c.S = S;
+                    c.W = W;
+                    c.ctas = ctas;
+                    c.a_bytes = a_bytes;
+                    c.b_bytes = b_bytes;
+                    c.a_pitch = da;
+                    c.b_pitch = db;
+                    c.ms.s[0] = {8 * wm, tm};
+                    c.ms.n = 1;
+                    c.ns.s[0] = {8 * wn, tn};
+                    c.ns.n = 1;
+                    c.memops = (int64_t)tiles * (8 * wm + 8 * wn) * K + 2 * M * N;
+                    c.ncls = 1;
+                    c.cls[0] = IaatClass{catalog_code(IAAT_FAM_DMMA, 8 * wm, 8 * wn), 0, W, tiles, tm, 0, 8 * wm, 0,
+                                         8 * wn, tn, 0, 0};
+                    best = c;
+                }
+            }
+        }
+    if (!best.ok) return false;
+    Plan &pl = out;
+    pl = Plan();
+    pl.ks = 1;
+    IaatKsParams &k = pl.ksp;
+    std::memset(&k, 0, sizeof k);
+    k.sC = r.sC;
+    k.batch = r.batch;
+    k.nunits = (r.batch + best.P - 1) / best.P;
+    k.M = (int)M;
+    k.N = (int)N;
+    k.K = (int)K;
+    k.ldc = (int)r.ldc;
+    k.P = best.P;
+    k.S = best.S;
+    k.kc = kc;
+    k.nchunks = nchunks;
+    k.n_compute_warps = best.W;
+    k.a_pitch = best.a_pitch;
+    k.b_pitch = best.b_pitch;
+    k.a_bytes = best.a_bytes;
+    k.b_bytes = best.b_bytes;
+    k.a_tx = (int)((int64_t)best.P * (AK ? M * 128 : (int64_t)kc * best.a_pitch * 8));
+    k.b_tx = (int)((int64_t)best.P * (BK ? N * 128 : (int64_t)kc * best.b_pitch * 8));
+    k.stage_bytes = best.a_bytes + best.b_bytes;
+    k.beta_zero = r.beta_zero;
+    k.c_vec = 1;
+    k.cplx = 1;
+    k.c_elt = 16;
+    k.nclasses = 1;
+    k.cls[0] = best.cls[0];
+    // tensor maps on the real (re, im) view: dims in doubles, strides in bytes
+    auto geo = [&](TmaGeo &g, int64_t rows, int64_t cols, int64_t ld, int64_t stride, bool kmaj, int pitch, int D) {
+        g.dim[0] = (uint64_t)(2 * rows);
+        g.dim[1] = (uint64_t)cols;
+        g.dim[2] = (uint64_t)r.batch;
+        g.stride[0] = (uint64_t)(ld * 16);
+        g.stride[1] = (uint64_t)((r.batch > 1 ? stride : ld * cols) * 16);
+        if (kmaj) {
+            g.box[0] = 16;  // 8 complex
+            g.box[1] = (uint32_t)D;
+        } else {
+            g.box[0] = (uint32_t)pitch;
+            g.box[1] = (uint32_t)kc;
+        }
+        g.box[2] = (uint32_t)best.P;
+        g.swizzle128 = kmaj ? 1 : 0;
+    };
+    geo(pl.tmA, rowsA, colsA, r.lda, r.sA, AK, best.a_pitch, (int)M);
+    geo(pl.tmB, rowsB, colsB, r.ldb, r.sB, BK, best.b_pitch, (int)N);
+    pl.family = IAAT_FAM_KS_DMMA;
+    pl.single = 1;
+    pl.ksd = 1;
+    pl.vec = 1;
+    pl.ctas = best.ctas;
+    pl.grid = (int)std::min<int64_t>(k.nunits, (int64_t)r.sm_count * best.ctas);
+    pl.block = (best.W + 1) * 32;
+    pl.smem = IAAT_KS_BAR_BYTES + 1024 + best.S * k.stage_bytes;
+    pl.nm = 1;
+    pl.nn = 1;
+    pl.mstrip[0] = best.ms.s[0];
+    pl.nstrip[0] = best.ns.s[0];
+    pl.memops = best.memops;
+    pl.est_cycles = best.unit;
+    pl.est_total = best.total;
+    pl.status = 0;
+    return true;
+}
+
 bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
 {
-    if (r.ptr_array || r.dtype > 1) return false;  // complex types: slab family only
+    if (r.ptr_array || r.dtype == 2) return false;  // complex fp32: slab family only
+    if (r.dtype == 3) return plan_ks_zdmma(r, kn, out);  // complex fp64: K-streamed DMMA (ZGEMM)
     const int elt = r.dtype == 0 ? 4 : 8;
     const int vw = 16 / elt, KU = vw, kc = 128 / elt;
     const int tidx = r.transA * 2 + r.transB;
@@ -1097,6 +1241,7 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
     k.beta_zero = r.beta_zero;
     k.c_vec = c_vec ? 1 : 0;
     k.ldgsts = ldgsts;
+    k.c_elt = elt;
     k.sA = r.sA;
     k.sB = r.sB;
     k.lda = (int)r.lda;

@@ -196,7 +196,7 @@ def tune_shape(sh, log):
         for (wm, wn) in ((1, 1), (1, 2), (2, 1), (2, 2)):
             for P in Ps:
                 trial(tile="%dx%d" % (8 * wm, 8 * wn), p=P, family=1)
-    if dtype == "f64" and M % 8 == 0 and N % 8 == 0:  # K-streamed DMMA warp tiles
+    if dtype in ("f64", "c64") and M % 8 == 0 and N % 8 == 0:  # K-streamed DMMA warp tiles (ZGEMM too)
         for a in range(1, 6):
             for bb in range(1, 6):
                 if a * bb <= 16 and 8 * a <= M and 8 * bb <= N:

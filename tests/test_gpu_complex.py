@@ -35,8 +35,8 @@ def test_complex_square_sweep(cdt, tr):
     for n in (5, 8, 13, 16, 24, 32, 40, 64, 80):
         if tr == "TN" and n > 32:
             continue
-        if cdt == np.complex128 and n > 56:
-            continue  # one 80^3 ZGEMM problem needs 2 x 102 KB of staged operands
+        if cdt == np.complex128 and n > 56 and n % 8:
+            continue  # large ZGEMM runs on the K-streamed DMMA kernels (M, N multiples of 8)
         for alpha, beta in ((1.5 - 0.5j, 0.25 + 1j), (-1j, 0)):
             c = CCase(cdt, tr[0], tr[1], n, n, n, 1203, 7, alpha, beta)
             if beta == 0:
@@ -67,3 +67,39 @@ def test_complex_irregular_and_quick_returns(cdt):
     torch.cuda.synchronize()
     assert torch.equal(before.view(torch.int64 if cdt == np.complex128 else torch.int32),
                        c.C.view(torch.int64 if cdt == np.complex128 else torch.int32))
+
+
+@pytest.mark.parametrize("tr", TRANS)
+def test_zgemm_k_streamed_dmma(tr):
+    """ZGEMM on the fp64 tensor cores (K-streamed DMMA over the real view,
+    forced family 3): every warp-tile size that divides the shape, ragged K
+    chunks (K % 8 != 0: the copy engine's zero fill), a ragged last unit,
+    complex alpha/beta with and without beta."""
+    import os
+    from paper_2208_09822_b200 import iaat
+    shapes = [(64, 64, 64), (80, 80, 80), (16, 24, 37), (40, 32, 9), (8, 8, 8)]
+    try:
+        for (M, N, K) in shapes:
+            if tr == "TN" and M * N * K > 32768:
+                continue
+            for wm in (1, 2, 4, 5):
+                for wn in (1, 2, 3, 5):
+                    if (M // 8) % wm or (N // 8) % wn:
+                        continue
+                    for beta, P in ((0j, 1), (0.5 - 0.25j, 2)):
+                        os.environ["IAAT_FORCE_FAMILY"] = "3"
+                        os.environ["IAAT_FORCE_TILE"] = "%dx%d" % (8 * wm, 8 * wn)
+                        os.environ["IAAT_FORCE_P"] = str(P)
+                        c = CCase(np.complex128, tr[0], tr[1], M, N, K, 97, 23, 1.25 + 0.5j, beta)
+                        p = iaat.iaat_plan_describe(3, tr[0], tr[1], M, N, K, c.lda, c.sA, c.ldb, c.sB, c.ldc, c.sC,
+                                                    c.batch, beta == 0)
+                        if p["family"] != "ks_dmma":
+                            continue
+                        if beta == 0:
+                            c.C.fill_(float("nan"))
+                        c.run()
+                        torch.cuda.synchronize()
+                        c.check(sample_ids(c.batch, 48, 24))
+    finally:
+        for k in ("IAAT_FORCE_FAMILY", "IAAT_FORCE_TILE", "IAAT_FORCE_P"):
+            os.environ.pop(k, None)
