@@ -93,7 +93,7 @@ def test_zgemm_k_streamed_dmma(tr):
                         c = CCase(np.complex128, tr[0], tr[1], M, N, K, 97, 23, 1.25 + 0.5j, beta)
                         p = iaat.iaat_plan_describe(3, tr[0], tr[1], M, N, K, c.lda, c.sA, c.ldb, c.sB, c.ldc, c.sC,
                                                     c.batch, beta == 0)
-                        if p["family"] != "ks_dmma":
+                        if p.get("family") != "ks_dmma":
                             continue
                         if beta == 0:
                             c.C.fill_(float("nan"))
