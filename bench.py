@@ -129,11 +129,11 @@ def workload(cfg):
         desc = ("cgemm sweep (SURVEY f1): complex fp32 M=N=K in {4,...,80} x {NN,NT,TT}, batch=floor(256MiB/(3n^2*8B)), "
                 "alpha=1.5-0.5i, beta=0.5+0.25i, seed 1; GFLOP/s by Eq. 2 (8MNK)")
     elif cfg == 7:  # complex fp64
-        for n in (8, 16, 24, 32, 40, 48, 56, 64, 72, 80):
+        for n in (8, 16, 24, 32, 40, 48, 64, 80):
             b = (256 * 1024 * 1024) // (3 * n * n * 16)
             for tr in ("NN", "NT", "TT"):
                 S.append(Shape("c64", tr, n, n, n, b, 1.5 - 0.5j, 0.5 + 0.25j, 1))
-        desc = ("zgemm sweep (SURVEY f1): complex fp64 M=N=K in {8,16,...,80} x {NN,NT,TT}, batch=floor(256MiB/(3n^2*16B)), "
+        desc = ("zgemm sweep (SURVEY f1): complex fp64 M=N=K in {8,16,24,32,40,48,64,80} x {NN,NT,TT}, batch=floor(256MiB/(3n^2*16B)), "
                 "alpha=1.5-0.5i, beta=0.5+0.25i, seed 1; GFLOP/s by Eq. 2 (8MNK)")
     else:
         raise SystemExit("unknown config %r" % cfg)

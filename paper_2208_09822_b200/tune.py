@@ -60,7 +60,7 @@ def config_shapes(cfg):
             for tr in ("NN", "NT", "TT"):
                 out.append(("c32", tr, n, n, n, (256 << 20) // (24 * n * n), 1.5 - 0.5j, 0.5 + 0.25j))
     elif cfg == 7:  # complex fp64 sweep (bench.py --config 7)
-        for n in (8, 16, 24, 32, 40, 48, 56, 64, 72, 80):
+        for n in (8, 16, 24, 32, 40, 48, 64, 80):
             for tr in ("NN", "NT", "TT"):
                 out.append(("c64", tr, n, n, n, (256 << 20) // (48 * n * n), 1.5 - 0.5j, 0.5 + 0.25j))
     return out

@@ -1,0 +1,4 @@
+cp paper_2208_09822_b200/tuning/b200.tsv gpurun_out/b200_t58.tsv
+timeout 1800 python -m paper_2208_09822_b200.tune --config 7 --min-n 56 --out gpurun_out/b200_t58.tsv --log gpurun_out/tune58.log > /dev/null 2>&1; echo tune=$?
+cp gpurun_out/b200_t58.tsv paper_2208_09822_b200/tuning/b200.tsv
+timeout 900 python bench.py --config 7 --steps 5 --warmup 3 --no-e2e > gpurun_out/bench58_c7.json 2>gpurun_out/bench58_c7.err; echo bench7=$?
