@@ -160,6 +160,10 @@ def test_catalog_register_budget():
         elif e["family"] == "fma":
             assert gen.fma_regs(e["dtype"], e["trans"], e["mr"], e["nr"]) <= gen.REG_BUDGET[e["dtype"]]
             assert 1 <= e["mr"] <= 8 and 1 <= e["nr"] <= 8
+        elif e["family"] == "ksu_fma":
+            assert e["dtype"] == "f32" and (e["mr"], e["nr"]) in gen.KSU_TILES
+        elif e["family"] == "ks_dmma" and e["dtype"] == "c64":
+            assert (e["mr"] // 8, e["nr"] // 8) in gen.KSZ_TILES
         elif e["family"] in ("ks_fma", "ks1_fma"):
             # K-streamed entries: only those the install-time register check
             # (tools/ks_regs.py -> gen/ks_unroll.json) accepted
