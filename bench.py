@@ -54,6 +54,27 @@ def peaks():
         return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
+def roofline_of(s, cnt, t, pk):
+    """Roofline object of one launch (shape s, cnt problems, t seconds):
+    HBM-bound -> algorithmic GB/s vs the measured copy bandwidth; otherwise
+    flops vs the derived FFMA (fp32, "alu") or DMMA (fp64, "tensor") peak."""
+    hbm_time = s.alg_bytes(cnt) / (pk["hbm_gbs"] * 1e9)
+    fp32 = s.dtype in ("f32", "c32")
+    cmp_peak = FFMA_PEAK_TFLOPS if fp32 else DMMA_PEAK_TFLOPS
+    if hbm_time >= s.flops(cnt) / (cmp_peak * 1e12):
+        roof = {"bound": "hbm", "achieved": round(s.alg_bytes(cnt) / t / 1e9, 1), "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": round(s.alg_bytes(cnt) / t / 1e9 / pk["hbm_gbs"], 4),
+                "peak_source": pk["source"]}
+    else:
+        roof = {"bound": "alu" if fp32 else "tensor", "achieved": round(s.flops(cnt) / t / 1e12, 2),
+                "peak": round(cmp_peak, 1), "unit": "TFLOP/s",
+                "frac": round(s.flops(cnt) / t / 1e12 / cmp_peak, 4),
+                "peak_source": ("derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md)" if fp32 else
+                                "derived: 148 SM x 64 FP64 FMA/clk (DMMA) x 2 x 1.965 GHz (DESIGN.md)")}
+    roof["traffic"] = load_traffic(s.name())
+    return roof
+
+
 # ---------------------------------------------------------------- workloads
 class Shape:
     def __init__(self, dtype, tr, M, N, K, batch, alpha, beta, seed):
@@ -129,12 +150,25 @@ def workload(cfg):
         desc = ("cgemm sweep (SURVEY f1): complex fp32 M=N=K in {4,...,80} x {NN,NT,TT}, batch=floor(256MiB/(3n^2*8B)), "
                 "alpha=1.5-0.5i, beta=0.5+0.25i, seed 1; GFLOP/s by Eq. 2 (8MNK)")
     elif cfg == 7:  # complex fp64
-        for n in (8, 16, 24, 32, 40, 48, 64, 80):
+        for n in (8, 16, 24, 32, 40, 48, 56, 64, 80):
             b = (256 * 1024 * 1024) // (3 * n * n * 16)
             for tr in ("NN", "NT", "TT"):
                 S.append(Shape("c64", tr, n, n, n, b, 1.5 - 0.5j, 0.5 + 0.25j, 1))
-        desc = ("zgemm sweep (SURVEY f1): complex fp64 M=N=K in {8,16,24,32,40,48,64,80} x {NN,NT,TT}, batch=floor(256MiB/(3n^2*16B)), "
+        desc = ("zgemm sweep (SURVEY f1): complex fp64 M=N=K in {8,16,24,32,40,48,56,64,80} x {NN,NT,TT}, batch=floor(256MiB/(3n^2*16B)), "
                 "alpha=1.5-0.5i, beta=0.5+0.25i, seed 1; GFLOP/s by Eq. 2 (8MNK)")
+    elif cfg == 8:  # fp32 TN above the paper's 32^3 bound (iaat_set_tn_limit)
+        for n in range(36, 81, 4):
+            b = (256 * 1024 * 1024) // (3 * n * n * 4)
+            S.append(Shape("f32", "TN", n, n, n, b, 1.5, 0.5, 1))
+        desc = ("fp32 TN above 32^3 (SURVEY f2, iaat_set_tn_limit(80^3)): M=N=K in {36,...,80}, "
+                "batch=floor(256MiB/(3n^2*4B)), alpha=1.5, beta=0.5, seed 1")
+    elif cfg == 9:  # fp64 TN / TT
+        for n in range(8, 81, 8):
+            b = (256 * 1024 * 1024) // (3 * n * n * 8)
+            for tr in ("TN", "TT"):
+                S.append(Shape("f64", tr, n, n, n, b, 1.5, 0.5, 1))
+        desc = ("fp64 TN/TT (SURVEY f2; TN above 32^3 via iaat_set_tn_limit(80^3)): M=N=K in {8,...,80}, "
+                "batch=floor(256MiB/(3n^2*8B)), alpha=1.5, beta=0.5, seed 1")
     else:
         raise SystemExit("unknown config %r" % cfg)
     return S, desc
@@ -202,6 +236,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     shapes, desc = workload(args.config)
+    if any(s.tr == "TN" and s.M * s.N * s.K > 32768 for s in shapes):
+        assert iaat.iaat_set_tn_limit(512000) == 0  # TN above the paper's 32^3
     stream = torch.cuda.current_stream()
     tdt = {"f32": torch.float32, "f64": torch.float64, "c32": torch.float32, "c64": torch.float64}
 
@@ -308,19 +344,7 @@ def run_ours(args, rank, world, local_rank):
                            "frac_roofline": round(t_roof / t, 4)})
     s, lo, cnt = chunks[dom]
     tdom = per_call_ms[dom] * 1e-3
-    hbm_time = s.alg_bytes(cnt) / (pk["hbm_gbs"] * 1e9)
-    cmp_peak = FFMA_PEAK_TFLOPS if s.dtype in ("f32", "c32") else DMMA_PEAK_TFLOPS
-    cmp_time = s.flops(cnt) / (cmp_peak * 1e12)
-    traffic = load_traffic(s.name())
-    if hbm_time >= cmp_time:
-        roof = {"bound": "hbm", "achieved": round(s.alg_bytes(cnt) / tdom / 1e9, 1), "peak": pk["hbm_gbs"],
-                "unit": "GB/s", "frac": round(s.alg_bytes(cnt) / tdom / 1e9 / pk["hbm_gbs"], 4),
-                "traffic": traffic, "peak_source": pk["source"]}
-    else:
-        roof = {"bound": "alu", "achieved": round(s.flops(cnt) / tdom / 1e12, 2), "peak": round(cmp_peak, 1),
-                "unit": "TFLOP/s", "frac": round(s.flops(cnt) / tdom / 1e12 / cmp_peak, 4),
-                "traffic": traffic,
-                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md)"}
+    roof = roofline_of(s, cnt, tdom, pk)
     roof["kernel"] = s.name()
     roof["share_of_step"] = round(per_call_ms[dom] / ms_step, 4)
     roof["bytes_per_launch"] = s.alg_bytes(cnt)
@@ -487,10 +511,15 @@ def run_chunked_config5(args, rank, world, local_rank, shapes, desc, chunks, buf
         t_roof = max(s.flops() / (DMMA_PEAK_TFLOPS * 1e12), s.alg_bytes() / (pk["hbm_gbs"] * 1e9))
         shapes_out.append({"shape": nm, "batch": cnt, "ms": round(ms, 4), "gflops": round(s.flops() / t / 1e9, 1),
                            "frac_roofline": round(t_roof / t, 4)})
+    nm, (ms, cnt, s) = max(res.items(), key=lambda kv: kv[1][0])
+    dom_roof = roofline_of(s, cnt, ms * 1e-3, pk)
+    dom_roof["kernel"] = nm
+    dom_roof["share_of_step"] = round(ms / total_ms, 4)
     return {"metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total_ms, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc}, "gpu_launches": int(n_launch), "clocks": clk, "shapes": shapes_out}
+            "config": {"workload": desc}, "roofline": dom_roof, "gpu_launches": int(n_launch), "clocks": clk,
+            "shapes": shapes_out}
 
 
 def run_e2e(args, chunks, bufs, call, stream, world):
@@ -679,7 +708,8 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2,
-                    help="BASELINE.json configs 1-5; 6/7 = complex fp32/fp64 sweeps (SURVEY f1)")
+                    help="BASELINE.json configs 1-5; 6/7 = complex fp32/fp64 sweeps (SURVEY f1); "
+                         "8/9 = fp32 TN above 32^3, fp64 TN/TT (SURVEY f2)")
     ap.add_argument("--cpu-frac", type=float, default=0.5)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")

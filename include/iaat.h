@@ -143,6 +143,16 @@ iaat_status_t iaat_zgemm_strided_batched(char transA, char transB, int64_t M, in
  * Host only, no GPU needed.  Negative sizes -> 0.                          */
 int iaat_is_small_gemm(char transA, char transB, int64_t M, int64_t N, int64_t K);
 
+/* TN domain extension.  The paper bounds TN at cbrt(MNK) <= 32
+ * because its NEON TN kernels cannot be vectorised; the
+ * GPU kernels have no such limit.  iaat_set_tn_limit raises (or restores) the
+ * M*N*K bound applied to transA='T', transB='N' calls, process-wide:
+ * max_mnk in [32768, 512000], else IAAT_ERROR_INVALID_VALUE and the limit
+ * is unchanged.  Default 32768 (the paper's domain).  iaat_is_small_gemm and
+ * every GEMM entry point follow the current value.                        */
+iaat_status_t iaat_set_tn_limit(int64_t max_mnk);
+int64_t iaat_get_tn_limit(void);
+
 /* Host only (no GPU needed): write, as JSON into json[0..cap), the plan the
  * strided call with these arguments would use (tile decomposition, tile
  * classes and their warps, problems per group, pipeline stages, grid, staging

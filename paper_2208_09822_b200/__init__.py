@@ -10,6 +10,7 @@ _NAMES = (
     "IAAT_R32F", "IAAT_R64F", "IAAT_C32F", "IAAT_C64F", "IaatError", "gemm_batched", "gemm_strided_batched",
     "iaat_catalog_describe", "iaat_gemm_batched", "iaat_gemm_grouped_strided", "iaat_gemm_strided_batched", "iaat_is_small_gemm",
     "iaat_last_cuda_error", "iaat_launch_count", "iaat_paper_tile", "iaat_plan_describe", "iaat_status_string",
+    "iaat_set_tn_limit", "iaat_get_tn_limit",
     "iaat_version",
 )
 

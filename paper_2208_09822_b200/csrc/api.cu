@@ -449,12 +449,26 @@ iaat_status_t iaat_dgemm_batched(char transA, char transB, int64_t M, int64_t N,
                              (const void *const *)Barray, ldb, &beta, (void *const *)Carray, ldc, batch, stream);
 }
 
+// TN domain limit: the paper's 32^3 bound for TN comes from the
+// NEON register file; the GPU kernels have no such reason,
+// so the caller may widen it up to the common 80^3 bound.
+static std::atomic<int64_t> g_tn_limit{32768};
+
+iaat_status_t iaat_set_tn_limit(int64_t max_mnk)
+{
+    if (max_mnk < 32768 || max_mnk > 512000) return IAAT_ERROR_INVALID_VALUE;
+    g_tn_limit.store(max_mnk);
+    return IAAT_SUCCESS;
+}
+
+int64_t iaat_get_tn_limit(void) { return g_tn_limit.load(); }
+
 int iaat_is_small_gemm(char transA, char transB, int64_t M, int64_t N, int64_t K)
 {
     // cbrt(MNK) <= 80, or <= 32 for TN -- integer form (reading A10)
     const int ta = parse_op(transA), tb = parse_op(transB);
     if (ta < 0 || tb < 0 || M < 0 || N < 0 || K < 0) return 0;
-    const int64_t lim = (ta == 1 && tb == 0) ? 32768 : 512000;
+    const int64_t lim = (ta == 1 && tb == 0) ? g_tn_limit.load() : 512000;
     if (M == 0 || N == 0 || K == 0) return 1;
     if (M > lim || N > lim || K > lim) return 0;
     return M * N * K <= lim ? 1 : 0;

@@ -847,8 +847,8 @@ bool plan_ks_zdmma(const PlanRequest &r, const Knobs &kn, Plan &out)
     const int da = AK ? 16 : zpitch(M), db = BK ? 16 : zpitch(N);
     const double hbm_per_problem = (double)(M * K + K * N + M * N * (r.beta_zero ? 1 : 2)) * 16;
     KsCand best;
-    for (int wm = 1; wm <= 5; ++wm)
-        for (int wn = 1; wn <= 5; ++wn) {
+    for (int wm = 1; wm <= 7; ++wm)  // the catalog decides which (wm, wn) exist
+        for (int wn = 1; wn <= 7; ++wn) {
             if ((M / 8) % wm || (N / 8) % wn) continue;
             if (kn.mr && (8 * wm != kn.mr || 8 * wn != kn.nr)) continue;
             if (!catalog_has(3, tidx, IAAT_FAM_KS_DMMA, 8 * wm, 8 * wn)) continue;
@@ -1154,8 +1154,8 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
         // fall into 4 different 32-byte bank windows
         auto dpitch = [](int64_t D) { int64_t q = D; while (q % 16 != 4) ++q; return (int)q; };
         const int da = AK ? kc : dpitch(M), db = BK ? kc : dpitch(N);
-        for (int wm = 1; wm <= 5; ++wm)
-            for (int wn = 1; wn <= 5; ++wn) {
+        for (int wm = 1; wm <= 7; ++wm)  // the catalog decides which (wm, wn) exist
+            for (int wn = 1; wn <= 7; ++wn) {
                 if ((M / 8) % wm || (N / 8) % wn) continue;
                 if (kn.mr && (8 * wm != kn.mr || 8 * wn != kn.nr)) continue;
                 if (!catalog_has(1, tidx, IAAT_FAM_KS_DMMA, 8 * wm, 8 * wn)) continue;

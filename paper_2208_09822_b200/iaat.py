@@ -31,7 +31,7 @@ EXPORTS = [
     "iaat_sgemm_strided_batched", "iaat_dgemm_strided_batched",
     "iaat_sgemm_batched", "iaat_dgemm_batched",
     "iaat_cgemm_strided_batched", "iaat_zgemm_strided_batched", "iaat_gemm_grouped_strided",
-    "iaat_is_small_gemm", "iaat_plan_describe", "iaat_catalog_describe", "iaat_paper_tile",
+    "iaat_is_small_gemm", "iaat_set_tn_limit", "iaat_get_tn_limit", "iaat_plan_describe", "iaat_catalog_describe", "iaat_paper_tile",
     "iaat_status_string", "iaat_last_cuda_error", "iaat_launch_count", "iaat_version",
 ]
 
@@ -55,6 +55,9 @@ def _load():
     lib.iaat_gemm_batched.restype = i
     lib.iaat_is_small_gemm.argtypes = [c, c, i64, i64, i64]
     lib.iaat_is_small_gemm.restype = i
+    lib.iaat_set_tn_limit.argtypes = [i64]
+    lib.iaat_set_tn_limit.restype = i
+    lib.iaat_get_tn_limit.restype = i64
     lib.iaat_plan_describe.argtypes = [i, c, c, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i, i,
                                        i64, i, ctypes.c_char_p, ctypes.c_size_t]
     lib.iaat_plan_describe.restype = i
@@ -112,6 +115,15 @@ def iaat_gemm_batched(dtype, transA, transB, M, N, K, alpha, Aarray, lda, Barray
 
 def iaat_is_small_gemm(transA, transB, M, N, K) -> bool:
     return bool(_lib.iaat_is_small_gemm(_ch(transA), _ch(transB), M, N, K))
+
+
+def iaat_set_tn_limit(max_mnk) -> int:
+    """Raise (or restore) the TN domain bound M*N*K <= max_mnk, 32768..512000."""
+    return _lib.iaat_set_tn_limit(max_mnk)
+
+
+def iaat_get_tn_limit() -> int:
+    return _lib.iaat_get_tn_limit()
 
 
 def iaat_plan_describe(dtype, transA, transB, M, N, K, lda, strideA, ldb, strideB, ldc, strideC, batch,

@@ -60,9 +60,16 @@ def config_shapes(cfg):
             for tr in ("NN", "NT", "TT"):
                 out.append(("c32", tr, n, n, n, (256 << 20) // (24 * n * n), 1.5 - 0.5j, 0.5 + 0.25j))
     elif cfg == 7:  # complex fp64 sweep (bench.py --config 7)
-        for n in (8, 16, 24, 32, 40, 48, 64, 80):
+        for n in (8, 16, 24, 32, 40, 48, 56, 64, 80):
             for tr in ("NN", "NT", "TT"):
                 out.append(("c64", tr, n, n, n, (256 << 20) // (48 * n * n), 1.5 - 0.5j, 0.5 + 0.25j))
+    elif cfg == 8:  # fp32 TN above 32^3 (bench.py --config 8; needs iaat_set_tn_limit)
+        for n in range(36, 81, 4):
+            out.append(("f32", "TN", n, n, n, (256 << 20) // (12 * n * n), 1.5, 0.5))
+    elif cfg == 9:  # fp64 TN / TT (bench.py --config 9)
+        for n in range(8, 81, 8):
+            for tr in ("TN", "TT"):
+                out.append(("f64", tr, n, n, n, (256 << 20) // (24 * n * n), 1.5, 0.5))
     return out
 
 
@@ -262,6 +269,9 @@ def main(argv=None):
     a = ap.parse_args(argv)
     sys.path.insert(0, ROOT)
     os.environ["IAAT_NO_TUNING"] = "1"  # tune against the cost model, not an older table
+    if set(a.config) & {8, 9}:
+        from paper_2208_09822_b200 import iaat
+        iaat.iaat_set_tn_limit(512000)  # TN above the paper's 32^3
     existing = {}
     if os.path.exists(a.out):
         for ln in open(a.out):

@@ -41,6 +41,28 @@ def test_small_predicate_matches_paper_examples():
     assert not iaat.iaat_is_small_gemm("N", "N", -1, 2, 2)
 
 
+def test_tn_limit_extension():
+    """the TN bound (paper: 32^3) can be widened up to 80^3 and
+    restored; out-of-range requests are rejected and change nothing."""
+    from paper_2208_09822_b200 import iaat
+    assert iaat.iaat_get_tn_limit() == 32768
+    assert not iaat.iaat_is_small_gemm("T", "N", 33, 32, 32)
+    assert iaat.iaat_set_tn_limit(32767) == 1 and iaat.iaat_set_tn_limit(512001) == 1
+    assert iaat.iaat_get_tn_limit() == 32768
+    try:
+        assert iaat.iaat_set_tn_limit(512000) == 0
+        assert iaat.iaat_is_small_gemm("T", "N", 80, 80, 80)
+        assert not iaat.iaat_is_small_gemm("T", "N", 81, 80, 80)
+        assert iaat.iaat_is_small_gemm("N", "T", 80, 80, 80)  # other transpositions unchanged
+        assert iaat.iaat_set_tn_limit(64000) == 0
+        assert iaat.iaat_is_small_gemm("T", "N", 40, 40, 40) and not iaat.iaat_is_small_gemm("T", "N", 41, 40, 40)
+        p = iaat.iaat_plan_describe(0, "T", "N", 40, 40, 40, 40, 1600, 40, 1600, 40, 1600, 1000)
+        assert p.get("family")
+    finally:
+        assert iaat.iaat_set_tn_limit(32768) == 0
+    assert not iaat.iaat_is_small_gemm("T", "N", 40, 40, 40)
+
+
 def test_status_strings_and_version():
     from paper_2208_09822_b200 import iaat
     for k, v in iaat.STATUS.items():

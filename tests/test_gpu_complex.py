@@ -32,7 +32,7 @@ def test_complex_brute_force_small(cdt, tr):
 @pytest.mark.parametrize("cdt", CDT)
 @pytest.mark.parametrize("tr", TRANS)
 def test_complex_square_sweep(cdt, tr):
-    for n in (5, 8, 13, 16, 24, 32, 40, 64, 80):
+    for n in (5, 8, 13, 16, 24, 32, 40, 56, 64, 80):
         if tr == "TN" and n > 32:
             continue
         if cdt == np.complex128 and n > 56 and n % 8:
@@ -44,6 +44,23 @@ def test_complex_square_sweep(cdt, tr):
             c.run()
             torch.cuda.synchronize()
             c.check(sample_ids(c.batch, 128, 64))
+
+
+@pytest.mark.parametrize("cdt", CDT)
+def test_complex_tn_extended_domain(cdt):
+    """complex TN above 32^3 once the caller widens the TN bound."""
+    from paper_2208_09822_b200 import iaat
+    assert iaat.iaat_set_tn_limit(512000) == 0
+    try:
+        for (M, N, K) in ((40, 40, 40), (64, 64, 64), (80, 80, 80), (37, 53, 61)):
+            if cdt == np.complex128 and (M % 8 or N % 8) and M * N * K > 175616:
+                continue  # large ZGEMM runs on the K-streamed DMMA kernels (M, N multiples of 8)
+            c = CCase(cdt, "T", "N", M, N, K, 301, 9, 1.5 - 0.5j, 0.25 + 1j)
+            c.run()
+            torch.cuda.synchronize()
+            c.check(sample_ids(c.batch, 96, 32))
+    finally:
+        iaat.iaat_set_tn_limit(32768)
 
 
 @pytest.mark.parametrize("cdt", CDT)

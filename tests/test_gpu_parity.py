@@ -124,6 +124,23 @@ def test_fp64_odd_shapes():
             c.check()
 
 
+@pytest.mark.parametrize("dtype", [F32, F64])
+def test_tn_extended_domain(dtype):
+    """TN above 32^3 once the caller widens the TN bound."""
+    from paper_2208_09822_b200 import iaat
+    big = Case(dtype, "T", "N", 40, 40, 40, 8, 5, 1.0, 0.0)
+    assert big.run(check=False) == 2  # IAAT_ERROR_NOT_SMALL by default
+    assert iaat.iaat_set_tn_limit(512000) == 0
+    try:
+        for (M, N, K) in [(33, 33, 33), (48, 48, 48), (64, 64, 64), (80, 80, 80), (79, 79, 79),
+                          (40, 72, 56), (1, 80, 80), (80, 3, 77), (68, 76, 52)]:
+            c = Case(dtype, "T", "N", M, N, K, 300, 43, 1.5, -0.5)
+            c.run()
+            c.check()
+    finally:
+        iaat.iaat_set_tn_limit(32768)
+
+
 # ---------------------------------------------------------------- full-size launch configs, sampled
 @pytest.mark.parametrize("n", [4, 16, 32, 64, 80])
 def test_config2_full_batch_sampled(n):
@@ -441,13 +458,13 @@ def test_ks_dmma_fp64_parity(tr):
     K % 4 != 0 -> the copy engine's zero fill feeds the last DMMA step),
     a ragged last unit, beta = 0 and beta != 0."""
     from paper_2208_09822_b200 import iaat
-    shapes = [(64, 64, 64), (80, 80, 80), (48, 32, 40), (16, 24, 37), (8, 8, 8)]
+    shapes = [(64, 64, 64), (80, 80, 80), (48, 32, 40), (16, 24, 37), (8, 8, 8), (56, 56, 56), (56, 16, 21)]
     try:
         for (M, N, K) in shapes:
             if tr == "TN" and M * N * K > 32768:
                 continue
-            for wm in (1, 2, 4, 5):
-                for wn in (1, 2, 3, 5):
+            for wm in (1, 2, 4, 5, 7):
+                for wn in (1, 2, 3, 5, 7):
                     if (M // 8) % wm or (N // 8) % wn:
                         continue
                     for beta, P in ((0.0, 1), (0.5, 2)):
