@@ -25,6 +25,12 @@
 #include "gen/kernel_table.inc"
 
 namespace iaat {
+bool pdl_enabled()
+{
+    static const bool on = std::getenv("IAAT_NO_PDL") == nullptr;
+    return on;
+}
+
 namespace {
 
 thread_local int g_last_cuda_error = 0;

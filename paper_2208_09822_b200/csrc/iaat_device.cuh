@@ -668,6 +668,39 @@ __device__ __forceinline__ void fma_class_loop(const IaatKParams &p, const IaatC
     }
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// The GEMM kernels are launched with programmatic stream serialisation
+// (launch_cfg in the generated launchers): the next call's grid may be
+// scheduled while this one drains, runs its prologue (mbarrier init), and
+// then waits in griddepcontrol.wait until every prerequisite grid has
+// completed and its memory is visible -- before touching any global
+// memory.  Each grid allows its dependents right after that wait.
+__device__ __forceinline__ void pdl_wait_and_release()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Host side: launch with programmatic stream serialisation (off when the
+// environment sets IAAT_NO_PDL, for A/B measurement; api.cu).
+bool pdl_enabled();
+
+template <typename... Args, typename... Act>
+cudaError_t launch_cfg(void (*kern)(Args...), int grid, int block, int smem, cudaStream_t s, Act &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<Act &&>(args)...);
+}
+
 // ------------------------------------------------------------------ kernel body
 // Dispatcher: generated by gen/generate.py (the install-time stage); its
 // static run() switches on the catalog code of the warp's class.
@@ -686,6 +719,7 @@ __device__ __forceinline__ void pipeline_kernel_body(const IaatKParams &p)
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait_and_release();
     if (warp == p.n_compute_warps) {
         producer_loop<T>(p, smem, full, empty, lane);
         return;

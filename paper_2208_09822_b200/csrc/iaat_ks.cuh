@@ -773,6 +773,7 @@ __device__ __forceinline__ void ks_kernel_body(const CUtensorMap *tmA, const CUt
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait_and_release();
     if (warp == p.n_compute_warps) {
         if (p.ldgsts)
             ks_producer_ldgsts<T, TA, TB>(p, smem, full, empty, lane);
