@@ -179,6 +179,39 @@ def test_integer_inputs_bitwise(dtype, tr):
     assert np.array_equal(got, ref)
 
 
+def test_dependent_calls_in_stream_order():
+    """Back-to-back calls on one stream where each reads the previous call's
+    C (programmatic dependent launch: the next grid may launch early but must
+    wait for its predecessor before reading).  Integer inputs keep every
+    value exact, so the chain is compared bitwise with int64 numpy; the
+    shapes alternate between the slab and the K-streamed families."""
+    from paper_2208_09822_b200 import iaat
+    rng = np.random.default_rng(45)
+    batch, n = 3000, 48
+    # entries in {-1, 0, 1}: after 4 products |value| <= 48^4 < 2^24, exact in fp32
+    A = rng.integers(-1, 2, (batch, n, n)).astype(np.float32)  # stored column-major: [b][col][row]
+    B = rng.integers(-1, 2, (batch, n, n)).astype(np.float32)
+    dX = torch.from_numpy(A).cuda().reshape(-1)
+    dB = torch.from_numpy(B).cuda().reshape(-1)
+    outs = [torch.empty_like(dX) for _ in range(4)]
+    ref = A.astype(np.int64)
+    Bi = B.astype(np.int64)
+    src = dX
+    for step, out in enumerate(outs):
+        # C_col[b] = X_col[b] @ B_col[b]; in [b][col][row] storage that is (B^T X^T)^T
+        _force(**({"family": 2} if step % 2 else {}))
+        try:
+            iaat.gemm_strided_batched("N", "N", n, n, n, 1.0, src, n, n * n, dB, n, n * n, 0.0, out, n, n * n, batch)
+        finally:
+            _force()
+        ref = np.einsum("bkr,bck->bcr", ref, Bi)  # X[b][k][r] * B[b][c][k] -> C[b][c][r]
+        src = out
+    torch.cuda.synchronize()
+    assert np.abs(ref).max() < 2 ** 24  # exact in fp32 all along
+    got = outs[-1].cpu().numpy().astype(np.int64).reshape(batch, n, n)
+    assert np.array_equal(got, ref)
+
+
 def test_transpose_identity_fp32_bitwise():
     """P7: op(A)op(B) = (op(B)^T op(A)^T)^T -- one k-ascending FFMA chain per
     element and fma(a,b,c) = fma(b,a,c) make the two calls bitwise equal."""
