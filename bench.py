@@ -531,7 +531,14 @@ def run_e2e(args, chunks, bufs, call, stream, world):
     import torch
     host = {}
     for key, (A, B, C) in bufs.items():
-        host[key] = tuple(t.cpu().pin_memory() for t in (A, B, C))
+        # pinned host copies filled straight from the device (no pageable
+        # intermediate: one rank per GPU would otherwise double its host RAM)
+        hs = []
+        for t in (A, B, C):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            hs.append(h)
+        host[key] = tuple(hs)
     steps = max(1, min(args.steps, args.e2e_steps))
     up, down = torch.cuda.Stream(), torch.cuda.Stream()
     last_down = [None]
