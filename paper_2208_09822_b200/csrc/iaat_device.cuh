@@ -681,6 +681,22 @@ __device__ __forceinline__ void pdl_wait_and_release()
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Host side: opt the kernel into IAAT_SMEM_LIMIT bytes of dynamic smem on the
+// current device, once per device (a single process may drive several GPUs,
+// SURVEY 8.5; the attribute belongs to each device's context).
+template <typename Kern>
+cudaError_t ensure_smem_attr(Kern kern, unsigned long long &done)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = dev < 64 ? 1ull << dev : 0ull;
+    if (bit && (__atomic_load_n(&done, __ATOMIC_ACQUIRE) & bit)) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, IAAT_SMEM_LIMIT);
+    if (e == cudaSuccess && bit) __atomic_fetch_or(&done, bit, __ATOMIC_RELEASE);
+    return e;
+}
+
 // Host side: launch with programmatic stream serialisation (off when the
 // environment sets IAAT_NO_PDL, for A/B measurement; api.cu).
 bool pdl_enabled();

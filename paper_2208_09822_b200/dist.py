@@ -32,3 +32,18 @@ def aggregate_gflops(flops_per_rank, times_s):
     """Whole-job GFLOP/s: total flops over the SLOWEST rank's time."""
     t = max(times_s)
     return sum(flops_per_rank) / t / 1e9 if t > 0 else 0.0
+
+
+def gemm_on_devices(calls):
+    """Single-process multi-GPU driver (SURVEY 8.5's process model): `calls`
+    is a list of (device_index, kwargs of iaat.gemm_strided_batched) whose
+    tensors live on that device.  Each call is enqueued on its device's
+    current stream (asynchronous; the library keeps per-device kernel
+    attributes and plans), and the list returns once everything is enqueued.
+    Use one shard per device from shard_range(); no data crosses devices."""
+    import torch
+
+    from . import iaat
+    for dev, kw in calls:
+        with torch.cuda.device(dev):
+            iaat.gemm_strided_batched(**kw)

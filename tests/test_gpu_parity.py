@@ -212,6 +212,27 @@ def test_dependent_calls_in_stream_order():
     assert np.array_equal(got, ref)
 
 
+def test_single_process_device_loop_matches_one_call():
+    """dist.gemm_on_devices: shards of one batch issued per device from one
+    process (here every shard on cuda:0, the only GPU) equal one
+    unsharded call bitwise."""
+    from paper_2208_09822_b200 import dist
+    n, batch = 40, 1001
+    one = Case(F32, "N", "T", n, n, n, batch, 61, 1.5, 0.5)
+    parts = Case(F32, "N", "T", n, n, n, batch, 61, 1.5, 0.5)
+    one.run()
+    A, B, C = parts.views()
+    calls = []
+    for g in range(3):
+        lo, hi = dist.shard_range(batch, g, 3)
+        calls.append((0, dict(transA="N", transB="T", M=n, N=n, K=n, alpha=1.5, A=A[lo * parts.sA:], lda=parts.lda,
+                              strideA=parts.sA, B=B[lo * parts.sB:], ldb=parts.ldb, strideB=parts.sB, beta=0.5,
+                              C=C[lo * parts.sC:], ldc=parts.ldc, strideC=parts.sC, batch=hi - lo)))
+    dist.gemm_on_devices(calls)
+    torch.cuda.synchronize()
+    assert bits_equal(one.views()[2][:batch * one.sC], C[:batch * parts.sC])
+
+
 def test_transpose_identity_fp32_bitwise():
     """P7: op(A)op(B) = (op(B)^T op(A)^T)^T -- one k-ascending FFMA chain per
     element and fma(a,b,c) = fma(b,a,c) make the two calls bitwise equal."""
