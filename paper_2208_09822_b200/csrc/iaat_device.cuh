@@ -627,8 +627,10 @@ __device__ __forceinline__ void fma_class_loop(const IaatKParams &p, const IaatC
         const int64_t b0 = g * p.P;
         const int np = (int)min((int64_t)p.P, p.batch - b0);
         const bool active = tile_ok && pl < np;
-        // A tile-contiguous iff !TA, B tile-contiguous iff TB (see load_frag)
-        RegTile<T, MR, NR, PairOf<T, !TA, TB, MR, NR>::value> acc;
+        // A tile-contiguous iff !TA, B tile-contiguous iff TB (see load_frag).
+        // TN with scalar loads (no 16-byte vectors): each a(i) is its own LDS,
+        // so the loads can land in register pairs along i -> FFMA2 as well
+        RegTile<T, MR, NR, PairOf<T, !TA || (!VEC && !TB), TB, MR, NR>::value> acc;
         acc.zero();
         mbar_wait(&full[s], (it / p.S) & 1);
         if (active) {
