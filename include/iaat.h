@@ -28,7 +28,12 @@
  *  - Execution is asynchronous on `stream` (a cudaStream_t; NULL = legacy
  *    default stream).  The call returns after enqueueing; buffers must stay
  *    alive until the stream's work completes.  Device faults surface at the
- *    caller's next synchronisation, as for any CUDA launch.
+ *    caller's next synchronisation, as for any CUDA launch.  Kernels are
+ *    launched with programmatic stream serialisation: a call's grid may
+ *    start its prologue while the previous kernel on the stream drains, but
+ *    it touches no global memory before that kernel has completed
+ *    (griddepcontrol.wait), so stream order is preserved exactly.  Set
+ *    IAAT_NO_PDL=1 in the environment to launch without it.
  *  - Validation happens before any launch.  On any error nothing is enqueued
  *    and C is untouched.  There is no CPU fallback: out-of-domain shapes
  *    return IAAT_ERROR_NOT_SMALL.
