@@ -724,31 +724,44 @@ __device__ __forceinline__ void ks_zdmma_class_loop(const IaatKsParams &p, const
         }
         if (active) {
             double *C = reinterpret_cast<double *>(p.C + (b0 + pl) * scb);
-            // per 8x8 block: its two C_in loads before its two stores (few live registers)
+            // blocks in pairs: the pair's four C_in loads before its four stores
+            // (stores may alias later loads, so each batch is one L2 round trip;
+            // pairs halve the round trips at four more live doubles)
+            // (single blocks for the largest tiles, whose accumulators leave no room)
+            constexpr int NBLK = WM * WN, NB = NBLK <= 8 ? 2 : 1;
 #pragma unroll
-            for (int mi = 0; mi < WM; ++mi)
+            for (int b0k = 0; b0k < NBLK; b0k += NB) {
+                double2 ci[NB][2];
+                double *q[NB];
 #pragma unroll
-                for (int nj = 0; nj < WN; ++nj) {
-                    double2 ci[2];
-                    double *q0 = C + 2 * ((row0 + 8 * mi + 2 * t) + (int64_t)(col0 + 8 * nj + g) * ldc);
-                    if (!beta_zero) {
-                        ci[0] = __ldcs(reinterpret_cast<const double2 *>(q0));
-                        ci[1] = __ldcs(reinterpret_cast<const double2 *>(q0 + 2));
+                for (int u = 0; u < NB; ++u) {
+                    const int bk = b0k + u < NBLK ? b0k + u : b0k;
+                    const int mi = bk / WN, nj = bk % WN;
+                    q[u] = C + 2 * ((row0 + 8 * mi + 2 * t) + (int64_t)(col0 + 8 * nj + g) * ldc);
+                    if (!beta_zero && b0k + u < NBLK) {
+                        ci[u][0] = __ldcs(reinterpret_cast<const double2 *>(q[u]));
+                        ci[u][1] = __ldcs(reinterpret_cast<const double2 *>(q[u] + 2));
                     }
+                }
+#pragma unroll
+                for (int u = 0; u < NB; ++u) {
+                    if (b0k + u >= NBLK) break;
+                    const int mi = (b0k + u) / WN, nj = (b0k + u) % WN;
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const double sr = re[mi][nj][h], si = im[mi][nj][h];
                         double tr = 0.0, tim = 0.0;
                         if (!beta_zero) {
-                            tr = fma_rn(br, ci[h].x, mul_rn(-bi, ci[h].y));
-                            tim = fma_rn(br, ci[h].y, mul_rn(bi, ci[h].x));
+                            tr = fma_rn(br, ci[u][h].x, mul_rn(-bi, ci[u][h].y));
+                            tim = fma_rn(br, ci[u][h].y, mul_rn(bi, ci[u][h].x));
                         }
                         double2 o;
                         o.x = fma_rn(ar, sr, fma_rn(-ai, si, tr));
                         o.y = fma_rn(ar, si, fma_rn(ai, sr, tim));
-                        __stcs(reinterpret_cast<double2 *>(q0 + 2 * h), o);
+                        __stcs(reinterpret_cast<double2 *>(q[u] + 2 * h), o);
                     }
                 }
+            }
         }
     }
 }
