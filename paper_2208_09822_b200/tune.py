@@ -196,10 +196,13 @@ def key_line(dt, tr, M, N, K, beta0):
                                                      int(beta0), vec)
 
 
-def tile_options(M, N):
-    ms = sorted({x for x in (1, 2, 3, 4, 5, 6, 7, 8) if x <= M and (x in (2, 4, 8) or x == M or M < 8)})
-    ns = sorted({x for x in (1, 2, 3, 4, 5, 6, 7, 8) if x <= N and (x in (2, 4, 8) or x == N or N < 8)})
-    return [(a, b) for a in ms for b in ns]
+def tile_options(M, N, wide=False):
+    """First-strip tile sizes to try.  wide: also 3, 5, 6 (the exact-cover
+    planner pairs them with a second strip), for the large fp32 shapes."""
+    base = (2, 3, 4, 5, 6, 8) if wide else (2, 4, 8)
+    ms = sorted({x for x in (1, 2, 3, 4, 5, 6, 7, 8) if x <= M and (x in base or x == M or M < 8)})
+    ns = sorted({x for x in (1, 2, 3, 4, 5, 6, 7, 8) if x <= N and (x in base or x == N or N < 8)})
+    return [(a, b) for a in ms for b in ns if not wide or a * b >= 12]
 
 
 def tune_shape(sh, log):
@@ -255,6 +258,13 @@ def tune_shape(sh, log):
                 for P in (1, 2, 3, 4):
                     for ctas in (1, 2, 3, 4):
                         trial(family=6, tile=tile, order=order, p=P, ctas=ctas)
+    if dtype == "f32" and min(M, N) >= 48:  # wider first-strip grid for the FFMA-bound sizes
+        for (mr, nr) in tile_options(M, N, wide=True):
+            if (mr, nr) in tile_options(M, N):
+                continue
+            for P in (1, 2, 3):
+                for csm in ((0, 1) if beta != 0 else (None,)):
+                    trial(tile="%dx%d" % (mr, nr), p=P, csmem=csm)
     if beta != 0:  # C_in from global (L2-prefetched) or staged in smem, both explicitly
         per_ab = (M * K + K * N) * elt
         for (mr, nr) in tile_options(M, N):
