@@ -20,6 +20,7 @@
 #include "iaat_device.cuh"
 #include "iaat_complex.cuh"
 #include "iaat_ks.cuh"
+#include "iaat_ksg.cuh"
 #include "planner.h"
 
 #include "gen/kernel_table.inc"
@@ -216,7 +217,8 @@ bool encode_tmap(CUtensorMap &m, const TmaGeo &g, const void *base, int elt)
     const cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(&m, elt == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
                     const_cast<void *>(base), g.dim, g.stride, g.box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                    g.swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                    g.swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : (g.swizzle64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE),
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -305,6 +307,24 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
     const Plan &plan = cached_plan(r);
     if (plan.status != 0) return (iaat_status_t)plan.status;
 
+    if (plan.ksg) {
+        IaatKsgParams kp = plan.kgp;
+        kp.alpha = a;
+        kp.beta = b;
+        alignas(64) CUtensorMap tmA, tmB, tmC;
+        if (!encode_tmap(tmA, plan.tmA, A, elt) || !encode_tmap(tmB, plan.tmB, B, elt) ||
+            !encode_tmap(tmC, plan.tmC, C, elt)) {
+            g_last_cuda_error = (int)cudaErrorInvalidValue;
+            return IAAT_ERROR_CUDA;
+        }
+        cudaError_t e = kLaunchKsg[plan.kg_entry].fn(tmA, tmB, tmC, kp, plan.grid, plan.smem, s);
+        if (e != cudaSuccess) {
+            g_last_cuda_error = (int)e;
+            return IAAT_ERROR_CUDA;
+        }
+        g_launches.fetch_add(1);
+        return IAAT_SUCCESS;
+    }
     if (plan.ks) {
         IaatKsParams kp = plan.ksp;
         static const int ks_debug = std::getenv("IAAT_DEBUG_KS") ? std::atoi(std::getenv("IAAT_DEBUG_KS")) : 0;

@@ -1,0 +1,466 @@
+// iaat_ksg.cuh -- the K-streamed "group" family (ksg): fp32 micro-kernels for
+// the upper half of the small-GEMM domain (n >= ~40), B200 sm_100a.
+//
+// Why a third family.  On B200 a CUDA-core FFMA GEMM is bound by the bytes
+// each lane pulls out of shared memory: the smem pipe delivers 128 B/clk
+// per SM whether or not lanes share addresses (a warp-wide LDS.128 costs
+// four wavefronts even as a broadcast), while the FMA pipes consume 128
+// FMA/clk.  A lane with an mr x nr register tile loads (mr + nr) words per
+// k-step for mr*nr FMAs, so at full FMA rate the smem pipe is
+// 4(mr + nr)/(mr nr) busy: 1.0 for 8x8, 1.2 for 10x5, 0.8 for 10x10 -- the
+// GPU form of the paper's "ratio of loads to FMAs", and
+// the reason the round-1 slab/ks kernels (8x8 and smaller private tiles)
+// stall at ~50 % of the FMA pipe for n >= 64.  ksg therefore runs the
+// largest register tiles that fit (up to 128 accumulators), and:
+//   * lane grids.  A warp owns one (LR*MR) x (LC*NR) block of ONE problem,
+//     lanes laid out LR x LC (LR * LC = 32) over its tiles (the LC lanes of
+//     a lane row share A fragments, the LR lanes of a lane column B
+//     fragments: broadcasts, no bank conflicts).
+//   * warp groups.  The consumer warps form G groups of W warps; each group
+//     owns its own S-stage ring, its own producer warp, its own C buffer
+//     and every G-th unit of P problems, so the groups drift apart and one
+//     group's epilogue overlaps the other groups' FFMA2 main loops (the
+//     ping-pang of PAPER.md:181 at the level of whole units).
+//   * C through shared memory.  The producer TMA-loads C_in of a unit into
+//     the group's C buffer while the unit's k loop runs, the epilogue
+//     updates it in place (C = alpha*acc + beta*C_in) and the producer
+//     TMA-stores the box: no lane waits on a global round trip, stores are
+//     whole 128-byte lines, and the buffer's column pitch is padded (free:
+//     the padding rows are out of the tensor, zero-filled on load and
+//     clipped on store) so the epilogue's smem accesses are conflict-free.
+//   * boundary by the copy engine.  The planner tiles an Mv x Nv problem
+//     (Mv >= M, Nv >= N); the TMA boxes cover Mv / Nv, so rows and columns
+//     past the problem arrive as zeros and are clipped from the C store --
+//     no predicated code anywhere.  The planner weighs those idle FMAs
+//     against the exact-tile families (it uses Mv = M, Nv = N whenever an
+//     exact lane grid exists: "no boundary processing").
+//
+// Staging (no pack pass): one 3-D TMA box per operand per
+// K-chunk of KC = 32 (128-byte swizzle) or 16 (64-byte swizzle) elements,
+// straight from the caller's layout.  Element maps of a lane's tile inside
+// its warp block (ti = lane % LR, tj = lane / LR):
+//   K-major dim (rows of op(A) when transA = T, columns of op(B) when
+//     transB = N):   element r at  t + L*r          (interleaved; consecutive
+//                    lanes read consecutive swizzled rows: conflict-free)
+//   MN-major dim:    element r at  V*(t + L*(r/V)) + r%V   (V-wide vector
+//                    groups, neighbouring lanes read neighbouring vectors)
+// Accumulation: one k-ascending FFMA (FFMA2 lane) chain per element, like
+// every other fp32 kernel of the library -- results are bitwise identical
+// across families and plans.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "iaat_device.cuh"
+#include "iaat_params.h"
+
+namespace iaat {
+namespace ksg {
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                            uint32_t bar, uint64_t policy)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, uint32_t src, int c0, int c1, int c2)
+{
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ float lds32(uint32_t a)
+{
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void lds64(uint32_t a, float &x, float &y)
+{
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x), "=f"(y) : "r"(a));
+}
+__device__ __forceinline__ void lds128(uint32_t a, float &x, float &y, float &z, float &w)
+{
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(a));
+}
+__device__ __forceinline__ void sts32(uint32_t a, float x) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(x) : "memory"); }
+__device__ __forceinline__ void sts64(uint32_t a, float x, float y)
+{
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x), "f"(y) : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t a, float x, float y, float z, float w)
+{
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+
+// Lane-grid geometry of one class.
+template <bool TA, bool TB, int MR, int NR, int LR>
+struct Geo {
+    static constexpr int LC = 32 / LR;
+    static constexpr bool AK = TA;   // op(A) K-major in smem
+    static constexpr bool BK = !TB;  // op(B) K-major in smem
+    static constexpr int VA = AK ? 1 : (MR % 4 == 0 ? 4 : (MR % 2 == 0 ? 2 : 1));
+    static constexpr int VB = BK ? 1 : (NR % 4 == 0 ? 4 : (NR % 2 == 0 ? 2 : 1));
+    // FFMA2 pairs along the dim whose fragments arrive as vectors
+    static constexpr int PAIR = (!AK && VA >= 2) ? 1 : ((!BK && VB >= 2) ? 2 : 0);
+    static constexpr int BR = LR * MR;  // warp block rows
+    static constexpr int BC = LC * NR;  // warp block columns
+    __device__ static __forceinline__ int row(int ti, int r) { return AK ? ti + LR * r : VA * (ti + LR * (r / VA)) + r % VA; }
+    __device__ static __forceinline__ int col(int tj, int c) { return BK ? tj + LC * c : VB * (tj + LC * (c / VB)) + c % VB; }
+};
+
+// Swizzled K-major row base: 16-byte chunk q of smem row ra (KC*4 bytes,
+// 128- or 64-byte TMA swizzle) lives at (kmaj_base(ra) ^ (q << 4)).
+template <int KC>
+__device__ __forceinline__ uint32_t kmaj_base(int ra)
+{
+    if (KC == 32) return ((uint32_t)ra << 7) | ((uint32_t)(ra & 7) << 4);
+    return ((uint32_t)ra << 6) | ((uint32_t)((ra >> 1) & 3) << 4);
+}
+
+// Fragment of one operand for one k-block of KU (2 or 4) k-steps: f[kk][r].
+// K-major: one LDS.64 / LDS.128 per element row (KU consecutive k values);
+// MN-major: one V-wide load per vector group per k-step.
+template <bool KMAJ, int R, int V, int L>
+struct Opnd {
+    uint32_t base[KMAJ ? R : 1];  // K-major: per-row swizzled base; MN-major: first element
+    uint32_t pitch;               // MN-major: bytes per k-step
+    template <int KU>
+    __device__ __forceinline__ void load(float (&f)[KU][R], uint32_t stage, int kb) const
+    {
+        if (KMAJ) {
+            const uint32_t q = (uint32_t)(kb >> 2) << 4, w = (uint32_t)(kb & 3) * 4u;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (KU == 4) lds128(stage + (base[r] ^ q), f[0][r], f[KU > 1 ? 1 : 0][r], f[KU > 2 ? 2 : 0][r], f[KU > 3 ? 3 : 0][r]);
+                else lds64(stage + (base[r] ^ q) + w, f[0][r], f[KU > 1 ? 1 : 0][r]);
+            }
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < KU; ++kk) {
+                const uint32_t a = stage + base[0] + (uint32_t)(kb + kk) * pitch;
+#pragma unroll
+                for (int g = 0; g < R / V; ++g) {
+                    const uint32_t ag = a + (uint32_t)(g * V * L * 4);
+                    if (V == 4) lds128(ag, f[kk][4 * g], f[kk][4 * g + 1], f[kk][4 * g + 2], f[kk][4 * g + 3]);
+                    else if (V == 2) lds64(ag, f[kk][2 * g], f[kk][2 * g + 1]);
+                    else f[kk][g] = lds32(ag);
+                }
+            }
+        }
+    }
+    // one k-step (ragged chunk tails)
+    __device__ __forceinline__ void load1(float (&f)[R], uint32_t stage, int k) const
+    {
+        if (KMAJ) {
+            const uint32_t q = (uint32_t)(k >> 2) << 4, w = (uint32_t)(k & 3) * 4u;
+#pragma unroll
+            for (int r = 0; r < R; ++r) f[r] = lds32(stage + (base[r] ^ q) + w);
+        } else {
+            const uint32_t a = stage + base[0] + (uint32_t)k * pitch;
+#pragma unroll
+            for (int r = 0; r < R; ++r) f[r] = lds32(a + (uint32_t)(((r / V) * V * L + r % V) * 4));
+        }
+    }
+};
+
+template <int KU, int MR, int NR, int PAIR>
+__device__ __forceinline__ void kblock_fma(RegTile<float, MR, NR, PAIR> &acc, const float (&a)[KU][MR],
+                                           const float (&b)[KU][NR])
+{
+#pragma unroll
+    for (int kk = 0; kk < KU; ++kk) acc.rank1([&](int i) { return a[kk][i]; }, [&](int j) { return b[kk][j]; });
+}
+
+// Shared-memory map: [barriers (1 KB)] then, per group g, at the first
+// 1024-byte boundary after them + g * group_bytes: S stages of
+// [A box | B box], then the C buffer (one TMA box [P][Nv][c_pitch] of C).
+struct Smem {
+    uint32_t ring;  // shared address of the group's stage 0
+    uint32_t cbuf;  // shared address of the group's C buffer
+    uint32_t full, empty, cfull, cready;  // shared addresses of the group's mbarriers
+    __device__ __forceinline__ Smem(unsigned char *smem, const IaatKsgParams &p, int g)
+    {
+        const uint32_t sbase = smem_u32(smem);
+        ring = ((sbase + IAAT_KSG_BAR_BYTES + 1023u) & ~1023u) + (uint32_t)g * (uint32_t)p.group_bytes;
+        cbuf = ring + (uint32_t)(p.S * p.stage_bytes);
+        full = sbase + (uint32_t)(g * IAAT_KSG_GROUP_BARS * 8);
+        empty = full + IAAT_KSG_MAX_STAGES * 8;
+        cfull = empty + IAAT_KSG_MAX_STAGES * 8;
+        cready = cfull + 8;
+    }
+};
+
+__device__ __forceinline__ void bar_init(uint32_t b, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint32_t b)
+{
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint32_t b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t b, uint32_t parity)
+{
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(b), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+
+// Consumer warp: one warp block of one problem per unit of its group.
+// DBG (experiment builds only; the library instantiates DBG = 0):
+//   bit 0: no A/B staging (consumers never wait for or release stages),
+//   bit 1: no epilogue (no C load / update / store).
+template <bool TA, bool TB, int MR, int NR, int LR, int KC, int KU, int G, int W, int DBG = 0>
+__device__ __forceinline__ void ksg_consumer(const IaatKsgParams &p, unsigned char *smem, int g, int w, int lane)
+{
+    typedef Geo<TA, TB, MR, NR, LR> Gm;
+    constexpr bool AK = Gm::AK, BK = Gm::BK;
+    const int K = p.K, nchunks = p.nchunks, S = p.S, Mv = p.Mv, Nv = p.Nv, cp = p.c_pitch;
+    const int64_t nunits = p.nunits;
+    const int ti = lane % LR, tj = lane / LR;
+    const int pl = w / p.wpp, blk = w - pl * p.wpp;
+    const int R0 = (blk % p.bm) * Gm::BR, C0 = (blk / p.bm) * Gm::BC;
+    const Smem sm(smem, p, g);
+
+    Opnd<AK, MR, Gm::VA, LR> oa;
+    Opnd<BK, NR, Gm::VB, Gm::LC> ob;
+    if (AK) {
+#pragma unroll
+        for (int r = 0; r < MR; ++r) oa.base[r] = kmaj_base<KC>(pl * Mv + R0 + Gm::row(ti, r));
+    } else {
+        oa.base[0] = (uint32_t)((pl * KC * p.a_pitch + R0 + Gm::VA * ti) * 4);
+    }
+    if (BK) {
+#pragma unroll
+        for (int c = 0; c < NR; ++c) ob.base[c] = kmaj_base<KC>(pl * Nv + C0 + Gm::col(tj, c));
+    } else {
+        ob.base[0] = (uint32_t)((pl * KC * p.b_pitch + C0 + Gm::VB * tj) * 4);
+    }
+    oa.pitch = (uint32_t)p.a_pitch * 4u;
+    ob.pitch = (uint32_t)p.b_pitch * 4u;
+    const float alpha = (float)p.alpha, beta = (float)p.beta;
+    const bool beta_zero = p.beta_zero != 0;
+    // this warp block's first C element in the group's C buffer
+    const uint32_t cb0 = sm.cbuf + (uint32_t)(((pl * Nv + C0) * cp + R0) * 4);
+
+    int s = 0;
+    uint32_t phase = 0, cphase = 0;
+    for (int64_t u = (int64_t)blockIdx.x * G + g; u < nunits; u += (int64_t)gridDim.x * G) {
+        RegTile<float, MR, NR, Gm::PAIR> acc;
+        acc.zero();
+        for (int ch = 0; ch < nchunks; ++ch) {
+            if (!(DBG & 1)) bar_wait(sm.full + 8 * s, phase);
+            const uint32_t sa = sm.ring + (uint32_t)(s * p.stage_bytes), sb = sa + (uint32_t)p.a_bytes;
+            const int kv = min(KC, K - ch * KC);
+            if (kv == KC) {
+                // register double buffering (the paper's ping-pang,
+                // PAPER.md:181): the fragments of k-block kb + KU load while
+                // the FFMA2s of kb issue
+                float fa[2][KU][MR], fb[2][KU][NR];
+                oa.template load<KU>(fa[0], sa, 0);
+                ob.template load<KU>(fb[0], sb, 0);
+#pragma unroll
+                for (int kb = 0; kb < KC; kb += KU) {
+                    const int cur = (kb / KU) & 1;
+                    if (kb + KU < KC) {
+                        oa.template load<KU>(fa[cur ^ 1], sa, kb + KU);
+                        ob.template load<KU>(fb[cur ^ 1], sb, kb + KU);
+                    }
+                    kblock_fma<KU, MR, NR, Gm::PAIR>(acc, fa[cur], fb[cur]);
+                }
+            } else {
+                int kb = 0;
+#pragma unroll 1
+                for (; kb + 4 <= kv; kb += 4) {
+                    float fa[4][MR], fb[4][NR];
+                    oa.template load<4>(fa, sa, kb);
+                    ob.template load<4>(fb, sb, kb);
+                    kblock_fma<4, MR, NR, Gm::PAIR>(acc, fa, fb);
+                }
+#pragma unroll 1
+                for (; kb < kv; ++kb) {
+                    float a1[MR], b1[NR];
+                    oa.load1(a1, sa, kb);
+                    ob.load1(b1, sb, kb);
+                    acc.rank1([&](int i) { return a1[i]; }, [&](int j) { return b1[j]; });
+                }
+            }
+            __syncwarp();
+            if (lane == 0 && !(DBG & 1)) bar_arrive(sm.empty + 8 * s);
+            if (++s == S) {
+                s = 0;
+                phase ^= 1u;
+            }
+        }
+        // fused epilogue in the group's C buffer (C_in already there when
+        // beta != 0): C = fma(alpha, acc, beta*C_in) -- the same two
+        // roundings as every other family's epilogue, so results stay
+        // bitwise identical across plans -- written back in place; the
+        // producer then TMA-stores the box.
+        if (DBG & 2) {
+            float v[MR][NR];
+            acc.get(v);
+            float t = 0.f;
+#pragma unroll
+            for (int c = 0; c < NR; ++c)
+#pragma unroll
+                for (int r = 0; r < MR; ++r) t += v[r][c];
+            if (t == 1234.5f) sts32(sm.cbuf, t);
+            continue;
+        }
+        bar_wait(sm.cfull, cphase);
+        cphase ^= 1u;
+        {
+            float v[MR][NR];
+            acc.get(v);
+#pragma unroll
+            for (int c = 0; c < NR; ++c) {
+                const uint32_t colb = cb0 + (uint32_t)(Gm::col(tj, c) * cp * 4);
+                if (!AK && Gm::VA >= 2) {
+#pragma unroll
+                    for (int g4 = 0; g4 < MR / Gm::VA; ++g4) {
+                        const uint32_t q = colb + (uint32_t)(Gm::row(ti, Gm::VA * g4) * 4);
+                        float ci[4] = {0.f, 0.f, 0.f, 0.f}, o[4];
+                        if (!beta_zero) {
+                            if (Gm::VA == 4) lds128(q, ci[0], ci[1], ci[2], ci[3]);
+                            else lds64(q, ci[0], ci[1]);
+                        }
+#pragma unroll
+                        for (int e = 0; e < Gm::VA; ++e) {
+                            const float x = v[Gm::VA * g4 + e][c];
+                            o[e] = beta_zero ? mul_rn(alpha, x) : fma_rn(alpha, x, mul_rn(beta, ci[e]));
+                        }
+                        if (Gm::VA == 4) sts128(q, o[0], o[1], o[2], o[3]);
+                        else sts64(q, o[0], o[1]);
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < MR; ++r) {
+                        const uint32_t q = colb + (uint32_t)(Gm::row(ti, r) * 4);
+                        const float x = v[r][c];
+                        sts32(q, beta_zero ? mul_rn(alpha, x) : fma_rn(alpha, x, mul_rn(beta, lds32(q))));
+                    }
+                }
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) bar_arrive(sm.cready);
+    }
+}
+
+// Producer warp of group g: lane 0 streams the group's units chunk by chunk,
+// and after each unit's chunks are queued it retires the previous unit's C
+// (TMA store once its epilogue is done) and brings in this unit's C_in.
+template <bool TA, bool TB, int KC, int G, int DBG = 0>
+__device__ __forceinline__ void ksg_producer(const IaatKsgParams &p, const CUtensorMap *tmA, const CUtensorMap *tmB,
+                                             const CUtensorMap *tmC, unsigned char *smem, int g, int lane)
+{
+    if (lane != 0) return;
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmC)) : "memory");
+    const uint64_t pol = policy_evict_first();
+    const uint32_t tx = (uint32_t)(p.a_tx + p.b_tx);
+    const Smem sm(smem, p, g);
+    int s = 0, it = 0;
+    uint32_t phase = 0, rphase = 0;
+    int prev_b0 = -1;
+    for (int64_t u = (int64_t)blockIdx.x * G + g; u < p.nunits; u += (int64_t)gridDim.x * G) {
+        const int b0 = (int)(u * p.P);
+        for (int c = 0; c < ((DBG & 1) ? 0 : p.nchunks); ++c, ++it) {
+            if (it >= p.S) bar_wait(sm.empty + 8 * s, phase);
+            const uint32_t st = sm.ring + (uint32_t)(s * p.stage_bytes), fb = sm.full + 8 * s;
+            bar_expect_tx(fb, tx);
+            const int k0 = c * KC;
+            if (TA) tma_load_3d(st, tmA, k0, 0, b0, fb, pol);
+            else tma_load_3d(st, tmA, 0, k0, b0, fb, pol);
+            if (TB) tma_load_3d(st + p.a_bytes, tmB, 0, k0, b0, fb, pol);
+            else tma_load_3d(st + p.a_bytes, tmB, k0, 0, b0, fb, pol);
+            if (++s == p.S) {
+                s = 0;
+                if (it >= 2 * p.S - 1) phase ^= 1u;
+            }
+        }
+        if (DBG & 2) continue;
+        if (prev_b0 >= 0) {
+            bar_wait(sm.cready, rphase);
+            rphase ^= 1u;
+            tma_store_3d(tmC, sm.cbuf, 0, 0, prev_b0);
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        if (!p.beta_zero) {
+            bar_expect_tx(sm.cfull, (uint32_t)p.c_tx);
+            tma_load_3d(sm.cbuf, tmC, 0, 0, b0, sm.cfull, pol);
+        } else {
+            bar_arrive(sm.cfull);
+        }
+        prev_b0 = b0;
+    }
+    if (prev_b0 >= 0 && !(DBG & 2)) {
+        bar_wait(sm.cready, rphase);
+        tma_store_3d(tmC, sm.cbuf, 0, 0, prev_b0);
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+}
+
+// The kernel body: 12 warps = three warpgroups.  Warpgroup 0 holds the
+// producers (warp g < G serves group g; the others retire at once) and
+// gives registers back (setmaxnreg.dec); warpgroups 1-2 are the G*W = 8
+// consumer warps, which take them (setmaxnreg.inc) for the big register
+// tiles.  Consumer c = warp - 4 is warp c % W of group c / W, so every SMSP
+// (warp % 4) hosts warps of two different groups.
+#define IAAT_KSG_THREADS IAAT_KSG_THREADS_HOST
+#define IAAT_KSG_PRODUCER_REGS 40
+#define IAAT_KSG_CONSUMER_REGS 232
+template <bool TA, bool TB, int MR, int NR, int LR, int KC, int KU, int G, int W, int DBG = 0>
+__device__ __forceinline__ void ksg_body(const IaatKsgParams &p, const CUtensorMap *tmA, const CUtensorMap *tmB,
+                                         const CUtensorMap *tmC)
+{
+    static_assert(G * W == 8, "ksg: two warpgroups of consumers");
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < G) {
+        const Smem sm(smem, p, threadIdx.x);
+        for (int s = 0; s < p.S; ++s) {
+            bar_init(sm.full + 8 * s, 1);
+            bar_init(sm.empty + 8 * s, W);
+        }
+        bar_init(sm.cfull, 1);
+        bar_init(sm.cready, W);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(IAAT_KSG_PRODUCER_REGS));
+        if (warp < G) ksg_producer<TA, TB, KC, G, DBG>(p, tmA, tmB, tmC, smem, warp, lane);
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(IAAT_KSG_CONSUMER_REGS));
+        const int c = warp - 4;
+        ksg_consumer<TA, TB, MR, NR, LR, KC, KU, G, W, DBG>(p, smem, c / W, c % W, lane);
+    }
+}
+
+}  // namespace ksg
+}  // namespace iaat

@@ -27,6 +27,7 @@ enum IaatFamily : int {
     IAAT_FAM_KS_DMMA = 3, // DMMA warp tiles, K-streamed TMA staging (fp64 only)
     IAAT_FAM_KS1_FMA = 4, // single-class K-streamed kernels (one per tile; the big tiles)
     IAAT_FAM_KSU_FMA = 6, // single-class K-streamed fp32, uniform swizzle phase only (tm/tn % 8 == 0)
+    IAAT_FAM_KSG = 7,     // fp32 lane-grid register tiles, warp groups, C through smem (iaat_ksg.cuh)
 };
 
 // One tile class: all tiles of one exact size (mr x nr) inside one row strip
@@ -114,4 +115,37 @@ struct IaatKsParams {
     int lda, ldb;
     int nclasses;
     IaatClass cls[IAAT_MAX_CLASSES];
+};
+
+// ---------------------------------------------------------------- K-streamed group family
+// Kernel executing plan of the "ksg" kernels (iaat_ksg.cuh): fp32, one
+// lane-grid tile class over an Mv x Nv "virtual" problem (Mv >= M, Nv >= N;
+// rows / columns past M / N are the copy engine's zero fill and are never
+// stored), G warp groups of W consumer warps (+ one producer warp per
+// group), each group with its own S-stage ring of K-chunks, its own C
+// buffer and every G-th unit of P problems.
+#define IAAT_KSG_MAX_STAGES 8
+#define IAAT_KSG_MAX_GROUPS 4
+#define IAAT_KSG_GROUP_BARS (2 * IAAT_KSG_MAX_STAGES + 2)  // full[S], empty[S], cfull, cready
+#define IAAT_KSG_BAR_BYTES 1024
+#define IAAT_KSG_THREADS_HOST 384  // == IAAT_KSG_THREADS (iaat_ksg.cuh): 3 warpgroups
+
+struct IaatKsgParams {
+    int64_t batch;
+    int64_t nunits;        // ceil(batch / P)
+    double alpha, beta;
+    int M, N, K;           // the problem
+    int Mv, Nv;            // the tiled (virtual) extent: Mv - M, Nv - N rows / columns of zero fill
+    int P, S, nchunks;     // problems per unit, stages per group ring, ceil(K / KC)
+    int a_pitch, b_pitch;  // MN-major operands: smem row pitch (elements) = TMA box inner dim
+    int c_pitch;           // C buffer: elements per column (TMA box inner dim >= Mv; padded against bank conflicts)
+    int a_bytes, b_bytes;  // smem bytes of one stage's A / B region (multiples of 1024)
+    int a_tx, b_tx;        // bytes one TMA box of A / B delivers (the full box, zero fill included)
+    int stage_bytes;       // a_bytes + b_bytes
+    int c_bytes;           // smem bytes of the group's C buffer (box [P][Nv][c_pitch], multiple of 1024)
+    int c_tx;              // bytes one TMA box of C delivers
+    int group_bytes;       // S * stage_bytes + c_bytes (one group's ring + C buffer)
+    int beta_zero;
+    int bm;                // warp blocks along Mv per problem
+    int wpp;               // warp blocks per problem (bm * blocks along Nv)
 };

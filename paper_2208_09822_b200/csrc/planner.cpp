@@ -342,6 +342,7 @@ struct Knobs {
 
 Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn);
 bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out);
+bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out);
 
 // ---------------------------------------------------------------- install-time tuning table
 // tuning/b200.tsv next to libiaat.so (written by paper_2208_09822_b200/tune.py on
@@ -388,6 +389,200 @@ const std::map<TunedKey, Knobs> &tuning_table()
     return table;
 }
 
+// ---------------------------------------------------------------- ksg family
+// (csrc/iaat_ksg.cuh).  One catalog entry = one kernel: a lane grid
+// lr x (32/lr) of mr x nr register tiles, warp blocks of (lr*mr) x
+// ((32/lr)*nr) elements of one problem, g groups of w consumer warps.  The
+// planner tiles the smallest Mv x Nv >= M x N that the entry's warp blocks
+// cover (Mv = M, Nv = N when the lane grid is exact; otherwise the copy
+// engine's zero fill supplies the rows / columns past M / N and the TMA
+// store clips them), sizes the stage ring to shared memory and picks the
+// entry with the lowest modelled time.
+
+// Shared-memory wavefronts of the epilogue's C-buffer accesses of one warp
+// for column pitch cp (128-bit accesses run in 4 phases of 8 lanes, 64-bit in
+// 2 of 16, 32-bit in 1 of 32; per phase the largest number of distinct words
+// in one bank).
+int ksg_epi_wavefronts(const IaatKsgCatalogEntry &e, int cp)
+{
+    const int LR = e.lr, LC = 32 / LR;
+    const bool AK = e.trans >= 2, BK = (e.trans & 1) == 0;
+    const int VA = AK ? 1 : (e.mr % 4 == 0 ? 4 : (e.mr % 2 == 0 ? 2 : 1));
+    const int VB = BK ? 1 : (e.nr % 4 == 0 ? 4 : (e.nr % 2 == 0 ? 2 : 1));
+    auto row = [&](int ti) { return AK ? ti : VA * ti; };
+    auto col = [&](int tj, int c) { return BK ? tj + LC * c : VB * (tj + LC * (c / VB)) + c % VB; };
+    const int V = (!AK && VA >= 2) ? VA : 1;
+    const int nph = V == 4 ? 4 : (V == 2 ? 2 : 1), per = 32 / nph;
+    int tot = 0;
+    for (int c = 0; c < e.nr; ++c)
+        for (int ph = 0; ph < nph; ++ph) {
+            int words[32][32];
+            int nb[32] = {0};
+            for (int l = ph * per; l < (ph + 1) * per; ++l) {
+                const int w0 = col(l / LR, c) * cp + row(l % LR);
+                for (int q = 0; q < V; ++q) {
+                    const int w = w0 + q, b = w & 31;
+                    bool seen = false;
+                    for (int x = 0; x < nb[b]; ++x) seen |= words[b][x] == w;
+                    if (!seen && nb[b] < 32) words[b][nb[b]++] = w;
+                }
+            }
+            int mx = 0;
+            for (int b = 0; b < 32; ++b) mx = std::max(mx, nb[b]);
+            tot += mx;
+        }
+    return tot;
+}
+
+bool ksg_default(const PlanRequest &r)
+{
+    return r.dtype == 0 && !r.ptr_array && std::min(r.M, r.N) >= 36 && r.K >= 16 &&
+           !(r.transA == 1 && r.transB == 0) && !std::getenv("IAAT_NO_KSG");
+}
+
+bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
+{
+    if (r.ptr_array || r.dtype != 0) return false;
+    const int elt = 4;
+    const int64_t M = r.M, N = r.N, K = r.K;
+    const bool AK = r.transA == 1, BK = r.transB == 0;
+    const int64_t colsA = AK ? M : K, colsB = BK ? N : K, rowsA = AK ? K : M, rowsB = BK ? K : N;
+    auto al16 = [&](int64_t el) { return (el * elt) % 16 == 0; };
+    if (K < 1 || r.batch < 1 || r.batch >= ((int64_t)1 << 31)) return false;
+    // the TMA store of C writes whole 16-byte granules along M (measured:
+    // rows M .. round_up(M, 4) - 1 of an ld-padded C were overwritten), so C
+    // columns must end on a granule boundary
+    if (M % 4) return false;
+    // TMA boxes for A, B and C: 16-byte aligned bases, ld's and strides, no broadcast strides
+    if (r.align % 16 || !al16(r.lda) || !al16(r.ldb) || !al16(r.ldc)) return false;
+    if (r.batch > 1 && (!al16(r.sA) || !al16(r.sB) || !al16(r.sC) || r.sA < r.lda * colsA ||
+                        r.sB < r.ldb * colsB || r.sC < r.ldc * N))
+        return false;
+    const int64_t lim = (int64_t)1 << 40;
+    if (r.sA * elt >= lim || r.sB * elt >= lim || r.sC * elt >= lim) return false;
+    const int tidx = r.transA * 2 + r.transB;
+    const int nent = (int)(sizeof(kKsgCatalog) / sizeof(kKsgCatalog[0]));
+    struct Cand {
+        int idx = -1, Mv = 0, Nv = 0, P = 0, S = 0, cp = 0, bm = 0, wpp = 0, stage = 0, cbytes = 0;
+        double cost = 0;
+    } best;
+    const double bytes = (double)(M * K + K * N + M * N * (r.beta_zero ? 1 : 2)) * elt;
+    for (int i = 0; i < nent; ++i) {
+        const IaatKsgCatalogEntry &e = kKsgCatalog[i];
+        if (e.trans != tidx) continue;
+        if (kn.fam == IAAT_FAM_KSG && kn.order >= 0 && kn.order != i) continue;
+        if (kn.mr && (e.mr != kn.mr || e.nr != kn.nr)) continue;
+        const int LC = 32 / e.lr, BR = e.lr * e.mr, BC = LC * e.nr;
+        const int Mv = (int)round_up(M, BR), Nv = (int)round_up(N, BC);
+        if (Mv > 256 || Nv > 256) continue;
+        const int bm = Mv / BR, wpp = bm * (Nv / BC);
+        if (wpp > e.w || e.w % wpp) continue;
+        const int P = e.w / wpp;
+        int cp = Mv, bestwf = 1 << 30;
+        for (int pad = 0; pad < 32 && Mv + pad <= 256; pad += 4) {
+            const int wf = ksg_epi_wavefronts(e, Mv + pad);
+            if (wf < bestwf) bestwf = wf, cp = Mv + pad;
+        }
+        const int a_tx = P * Mv * e.kc * elt, b_tx = P * Nv * e.kc * elt, c_tx = P * Nv * cp * elt;
+        const int stage = (int)(round_up(a_tx, 1024) + round_up(b_tx, 1024)), cbytes = (int)round_up(c_tx, 1024);
+        int S = 0;
+        while (S < IAAT_KSG_MAX_STAGES && IAAT_KSG_BAR_BYTES + 1024 + e.g * ((S + 1) * stage + cbytes) <= IAAT_SMEM_LIMIT)
+            ++S;
+        if (kn.fam == IAAT_FAM_KSG && kn.s > 0) S = std::min(S, kn.s);
+        if (S < 1) continue;
+        // model: FFMA2 work on the Mv x Nv tile (plain FFMA without a vector
+        // operand to pair), against the HBM time of the real bytes; the
+        // shorter of the two is partly exposed, and a one-stage ring or a
+        // smem-hungry tile (4(mr+nr)/(mr nr) words per FMA) costs extra
+        const bool pair = (!AK && e.mr % 2 == 0) || (!BK && e.nr % 2 == 0);
+        const double fma = (double)Mv * Nv * K / (128.0 * (pair ? 0.68 : 0.5));
+        const double smemf = 4.0 * (e.mr + e.nr) / (e.mr * e.nr);
+        const double hbm = bytes / 22.0;
+        double t = std::max(fma * std::max(1.0, smemf / 0.9), hbm) + 0.35 * std::min(fma, hbm);
+        if (S == 1) t *= 1.2;
+        if (best.idx < 0 || t < best.cost) {
+            best.idx = i;
+            best.Mv = Mv;
+            best.Nv = Nv;
+            best.P = P;
+            best.S = S;
+            best.cp = cp;
+            best.bm = bm;
+            best.wpp = wpp;
+            best.stage = stage;
+            best.cbytes = cbytes;
+            best.cost = t;
+        }
+    }
+    if (best.idx < 0) return false;
+    const IaatKsgCatalogEntry &e = kKsgCatalog[best.idx];
+    Plan pl;
+    IaatKsgParams &k = pl.kgp;
+    k.batch = r.batch;
+    k.nunits = (r.batch + best.P - 1) / best.P;
+    k.M = (int)M;
+    k.N = (int)N;
+    k.K = (int)K;
+    k.Mv = best.Mv;
+    k.Nv = best.Nv;
+    k.P = best.P;
+    k.S = best.S;
+    k.nchunks = (int)((K + e.kc - 1) / e.kc);
+    k.a_pitch = best.Mv;
+    k.b_pitch = best.Nv;
+    k.c_pitch = best.cp;
+    k.a_tx = best.P * best.Mv * e.kc * elt;
+    k.b_tx = best.P * best.Nv * e.kc * elt;
+    k.a_bytes = (int)round_up(k.a_tx, 1024);
+    k.b_bytes = (int)round_up(k.b_tx, 1024);
+    k.stage_bytes = best.stage;
+    k.c_tx = best.P * best.Nv * best.cp * elt;
+    k.c_bytes = best.cbytes;
+    k.group_bytes = best.S * best.stage + best.cbytes;
+    k.beta_zero = r.beta_zero;
+    k.bm = best.bm;
+    k.wpp = best.wpp;
+    auto geo = [&](TmaGeo &g, int64_t rows, int64_t cols, int64_t ld, int64_t stride, bool kmaj, int D) {
+        g.dim[0] = (uint64_t)rows;
+        g.dim[1] = (uint64_t)cols;
+        g.dim[2] = (uint64_t)r.batch;
+        g.stride[0] = (uint64_t)(ld * elt);
+        g.stride[1] = (uint64_t)((r.batch > 1 ? stride : round_up(ld * cols, 4)) * elt);
+        if (kmaj) {
+            g.box[0] = (uint32_t)e.kc;
+            g.box[1] = (uint32_t)D;
+        } else {
+            g.box[0] = (uint32_t)D;
+            g.box[1] = (uint32_t)e.kc;
+        }
+        g.box[2] = (uint32_t)best.P;
+        g.swizzle128 = kmaj && e.kc == 32 ? 1 : 0;
+        g.swizzle64 = kmaj && e.kc == 16 ? 1 : 0;
+    };
+    geo(pl.tmA, rowsA, colsA, r.lda, r.sA, AK, best.Mv);
+    geo(pl.tmB, rowsB, colsB, r.ldb, r.sB, BK, best.Nv);
+    pl.tmC.dim[0] = (uint64_t)M;
+    pl.tmC.dim[1] = (uint64_t)N;
+    pl.tmC.dim[2] = (uint64_t)r.batch;
+    pl.tmC.stride[0] = (uint64_t)(r.ldc * elt);
+    pl.tmC.stride[1] = (uint64_t)((r.batch > 1 ? r.sC : round_up(r.ldc * N, 4)) * elt);
+    pl.tmC.box[0] = (uint32_t)best.cp;
+    pl.tmC.box[1] = (uint32_t)best.Nv;
+    pl.tmC.box[2] = (uint32_t)best.P;
+    pl.ksg = 1;
+    pl.kg_entry = best.idx;
+    pl.family = IAAT_FAM_KSG;
+    pl.vec = 1;
+    pl.ctas = 1;
+    pl.grid = (int)std::min<int64_t>((k.nunits + e.g - 1) / e.g, (int64_t)r.sm_count);
+    pl.block = IAAT_KSG_THREADS_HOST;
+    pl.smem = IAAT_KSG_BAR_BYTES + 1024 + e.g * k.group_bytes;
+    pl.est_total = best.cost;
+    pl.status = 0;
+    out = pl;
+    return true;
+}
+
 Plan make_plan(const PlanRequest &r)
 {
     Knobs kn;
@@ -428,9 +623,36 @@ Plan make_plan(const PlanRequest &r)
         Plan pd;
         if (plan_ks(r, kd, pd)) return pd;
     }
+    if (kn.fam == IAAT_FAM_KSG) {
+        Plan pg;
+        if (plan_ksg(r, kn, pg)) {
+            pg.tuned = tuned;
+            return pg;
+        }
+        kn = Knobs();
+    }
+    if (!kn.any() && ksg_default(r)) {
+        // the upper half of the fp32 domain: lane-grid register tiles with
+        // warp groups (csrc/iaat_ksg.cuh) whenever their TMA preconditions hold
+        Plan pg;
+        if (plan_ksg(r, Knobs(), pg)) return pg;
+    }
     Plan p = make_plan_knobs(r, kn);
     if (p.status != 0 && kn.any()) p = make_plan_knobs(r, Knobs());
     else p.tuned = tuned;
+    if (p.status != 0 && !kn.any()) {
+        // shapes the slab family cannot stage (e.g. 16 x 16 x 2000: one
+        // problem's span exceeds shared memory) stream through the
+        // K-streamed families instead
+        Knobs kk;
+        kk.fam = (r.dtype == 1 || r.dtype == 3) ? IAAT_FAM_KS_DMMA : IAAT_FAM_KS_FMA;
+        Plan pk;
+        if (plan_ks(r, kk, pk)) return pk;
+        if (kk.fam == IAAT_FAM_KS_DMMA) {
+            kk.fam = IAAT_FAM_KS_FMA;
+            if (plan_ks(r, kk, pk)) return pk;
+        }
+    }
     return p;
 }
 
@@ -1304,6 +1526,17 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
     }
     const IaatKParams &k = p.kp;
     add("\"tuned\": %d, ", p.tuned);
+    if (p.ksg) {
+        const IaatKsgParams &q = p.kgp;
+        const IaatKsgCatalogEntry &e = kKsgCatalog[p.kg_entry];
+        add("\"family\": \"ksg\", \"entry\": %d, \"mr\": %d, \"nr\": %d, \"lane_rows\": %d, \"kc\": %d, "
+            "\"ku\": %d, \"groups\": %d, \"warps_per_group\": %d, \"Mv\": %d, \"Nv\": %d, \"P\": %d, \"S\": %d, "
+            "\"c_pitch\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, \"nunits\": %lld, \"est\": %.0f, ",
+            p.kg_entry, e.mr, e.nr, e.lr, e.kc, e.ku, e.g, e.w, q.Mv, q.Nv, q.P, q.S, q.c_pitch, p.grid, p.block,
+            p.smem, (long long)q.nunits, p.est_total);
+        s += "\"classes\": []}";
+        return s;
+    }
     const int ncls = p.ks ? p.ksp.nclasses : k.nclasses;
     const IaatClass *cls = p.ks ? p.ksp.cls : k.cls;
     if (p.ks) {

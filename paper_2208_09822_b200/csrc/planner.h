@@ -35,6 +35,7 @@ struct TmaGeo {
     uint64_t stride[2];   // bytes: ld * elt, problem stride * elt
     uint32_t box[3];      // box extents (elements)
     int swizzle128;       // 1: CU_TENSOR_MAP_SWIZZLE_128B (K-major operand)
+    int swizzle64;        // 1: CU_TENSOR_MAP_SWIZZLE_64B (K-major operand, 16-element K-chunks)
 };
 
 struct Plan {
@@ -45,6 +46,10 @@ struct Plan {
     int ksd = 0;           // K-streamed: 1 = fp64 DMMA warp-tile kernel (iaat_ksd_*)
     IaatKsParams ksp{};
     TmaGeo tmA{}, tmB{};
+    int ksg = 0;           // 1: ksg family (kgp + tmA/tmB/tmC, kernel kKsgCatalog[kg_entry])
+    int kg_entry = -1;
+    IaatKsgParams kgp{};
+    TmaGeo tmC{};
     int grid = 0, block = 0, smem = 0;
     int vec = 0;           // kernel variant: 16-byte vector paths enabled
     int family = 0;        // IAAT_FAM_FMA or IAAT_FAM_DMMA

@@ -326,6 +326,74 @@ def tune_shape(sh, log):
     return best_kw, best_p
 
 
+def line_to_knobs(v):
+    """Inverse of knobs_to_line: a table entry's fields as IAAT_FORCE_* knobs."""
+    mr, nr, P, S, ctas, order, fam, csm = (int(x) for x in v.split()[:8])
+    kw = {}
+    if mr:
+        kw["tile"] = "%dx%d" % (mr, nr)
+    for k, x, none in (("p", P, 0), ("s", S, 0), ("ctas", ctas, 0), ("order", order, -1), ("family", fam, -1),
+                       ("csmem", csm, -1)):
+        if x != none:
+            kw[k] = x
+    return kw
+
+
+def tune_ksg(sh, current, log):
+    """ksg family (csrc/iaat_ksg.cuh) against the current plan of one input:
+    every applicable catalog entry (forced), each at its planner-chosen ring
+    depth and one stage fewer, plus the current table entry (or the cost
+    model's plan); the leaders are re-timed and the fastest is kept."""
+    from paper_2208_09822_b200 import iaat
+    dtype, tr, M, N, K, batch, alpha, beta = sh
+    b = Bench(*sh)
+    cands = [current or {}]
+    for e in iaat.iaat_catalog_describe():
+        if e["family"] != "ksg" or e["trans"] != tr:
+            continue
+        set_knobs(family=7, order=e["index"])
+        try:
+            p = b.plan()
+        finally:
+            set_knobs()
+        if p.get("family") != "ksg" or p.get("entry") != e["index"]:
+            continue
+        cands.append({"family": 7, "order": e["index"]})
+        if p["S"] > 1:
+            cands.append({"family": 7, "order": e["index"], "s": p["S"] - 1})
+    res = []
+    for kw in cands:
+        set_knobs(**kw)
+        try:
+            p = b.plan()
+            if p["status"] == 0:
+                res.append((b.time_us(), kw, p))
+        except Exception as ex:  # a candidate that cannot run is skipped, not fatal
+            log("  candidate %s failed: %s" % (kw, ex))
+        finally:
+            set_knobs()
+    res.sort(key=lambda x: x[0])
+    final = []
+    for us, kw, p in res[:4] + [r for r in res if r[1] == cands[0]][:1]:
+        set_knobs(**kw)
+        try:
+            final.append((min(b.time_us(reps=12), b.time_us(reps=12)), kw, p))
+        except Exception as ex:
+            log("  candidate %s failed: %s" % (kw, ex))
+        finally:
+            set_knobs()
+    final.sort(key=lambda x: x[0])
+    cur = next((us for us, kw, p in final if kw == cands[0]), float("inf"))
+    best_us, best_kw, best_p = final[0]
+    b.free()
+    if best_kw != cands[0] and best_us > cur * 0.99:
+        best_kw, best_us, best_p = cands[0], cur, None
+    byts = (M * K + K * N + M * N * (1 if beta == 0 else 2)) * 4 * b.batch
+    log("ksg %s %dx%dx%d batch=%d current=%.1fus best=%.1fus (%.0f GB/s) knobs=%s" % (
+        tr, M, N, K, b.batch, cur, best_us, byts / best_us / 1e3, best_kw))
+    return best_kw, best_p
+
+
 def knobs_to_line(kw, p):
     """Knobs of the winning plan as the planner's table fields."""
     mr, nr = (int(x) for x in kw["tile"].split("x")) if "tile" in kw else (0, 0)
@@ -340,6 +408,7 @@ def main(argv=None):
     ap.add_argument("--log", default=None)
     ap.add_argument("--min-n", type=int, default=0, help="only inputs with max(M,N,K) >= this")
     ap.add_argument("--max-n", type=int, default=1 << 30)
+    ap.add_argument("--ksg", action="store_true", help="only compare the ksg family against the current entries")
     a = ap.parse_args(argv)
     sys.path.insert(0, ROOT)
     os.environ["IAAT_NO_TUNING"] = "1"  # tune against the cost model, not an older table
@@ -366,9 +435,14 @@ def main(argv=None):
         for sh in config_shapes(cfg):
             if not a.min_n <= max(sh[2:5]) <= a.max_n:
                 continue
-            kw, p = tune_shape(sh, log)
             dtype, tr, M, N, K, batch, alpha, beta = sh
             key = key_line({"f32": 0, "f64": 1, "c32": 2, "c64": 3}[dtype], tr, M, N, K, beta == 0)
+            if a.ksg:
+                if dtype != "f32" or tr == "TN":
+                    continue
+                kw, p = tune_ksg(sh, line_to_knobs(existing[key]) if key in existing else {}, log)
+            else:
+                kw, p = tune_shape(sh, log)
             if kw:
                 existing[key] = knobs_to_line(kw, p)
             else:

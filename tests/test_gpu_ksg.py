@@ -1,0 +1,119 @@
+"""GPU parity of the ksg family (csrc/iaat_ksg.cuh: lane-grid register
+tiles, warp groups, C through shared memory, TMA zero fill past M / N).
+
+Every catalog entry is forced (IAAT_FORCE_FAMILY=7, IAAT_FORCE_ORDER=entry)
+on exact and zero-filled (Mv > M, Nv > N) tilings, ragged K chunks (K % KC,
+K % 4 != 0), a ragged last unit (batch % P), beta != 0 and beta == 0 with a
+NaN-filled C, and compared element-wise with the oracle
+and bitwise with the slab family (one k-ascending FFMA chain per element and
+the same fused epilogue in every family, reading A7).
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from tests.gpu_utils import Case, sample_ids
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+F32 = np.float32
+
+
+def _force(**kw):
+    for k in ("IAAT_FORCE_FAMILY", "IAAT_FORCE_TILE", "IAAT_FORCE_P", "IAAT_FORCE_CTAS", "IAAT_FORCE_ORDER",
+              "IAAT_FORCE_S"):
+        os.environ.pop(k, None)
+    for k, v in kw.items():
+        os.environ["IAAT_FORCE_" + k.upper()] = str(v)
+
+
+def _entries():
+    from paper_2208_09822_b200 import iaat
+    return [e for e in iaat.iaat_catalog_describe() if e["family"] == "ksg"]
+
+
+def bits_equal(a, b):
+    return torch.equal(a.view(torch.int32), b.view(torch.int32))
+
+
+SHAPES = [(40, 40, 40), (48, 48, 48), (56, 56, 56), (64, 64, 64), (72, 72, 72), (80, 80, 80),
+          (76, 76, 76), (44, 52, 37), (61, 70, 50), (80, 36, 100), (33, 64, 130), (68, 76, 98)]
+
+
+def _plan(c, beta):
+    from paper_2208_09822_b200 import iaat
+    return iaat.iaat_plan_describe(0, c.tA, c.tB, c.M, c.N, c.K, c.lda, c.sA, c.ldb, c.sB, c.ldc, c.sC,
+                                   c.batch, beta == 0)
+
+
+@pytest.mark.parametrize("tr", ["NN", "NT", "TT"])
+def test_ksg_every_entry_parity_and_bitwise_vs_slab(tr):
+    ents = [e for e in _entries() if e["trans"] == tr]
+    assert ents, "no ksg entries for %s" % tr
+    ran = 0
+    try:
+        for e in ents:
+            for (M, N, K) in SHAPES:
+                for beta in (0.5, 0.0):
+                    _force(family=7, order=e["index"])
+                    c = Case(F32, tr[0], tr[1], M, N, K, 301, 31, 1.5, beta, ld_multiple=4)
+                    p = _plan(c, beta)
+                    if p.get("family") != "ksg" or p.get("entry") != e["index"]:
+                        continue
+                    A, B, C = c.views()
+                    if beta == 0:
+                        C.fill_(float("nan"))  # C is write-only at beta == 0 (reading A3)
+                    c.run()
+                    torch.cuda.synchronize()
+                    c.check(sample_ids(c.batch, 48, 24))
+                    got = C.clone()
+                    _force(family=0)
+                    c2 = Case(F32, tr[0], tr[1], M, N, K, 301, 31, 1.5, beta, ld_multiple=4)
+                    if beta == 0:
+                        c2.views()[2].fill_(float("nan"))
+                    c2.run()
+                    torch.cuda.synchronize()
+                    assert bits_equal(got, c2.views()[2]), (tr, e, M, N, K, beta)
+                    ran += 1
+    finally:
+        _force()
+    assert ran >= 2 * len(ents), ran
+
+
+def test_ksg_padding_and_gaps_untouched():
+    """ld > rows and gapped problem strides: the TMA store writes exactly
+    the M x N elements of every problem (NaN sentinels in the gaps stay)."""
+    try:
+        for tr in ("NN", "NT", "TT"):
+            _force(family=7)
+            c = Case(F32, tr[0], tr[1], 76, 72, 64, 257, 5, 1.0, 0.25, pad=4, spad=12)
+            p = _plan(c, 0.25)
+            assert p["family"] == "ksg", p
+            c.run()
+            torch.cuda.synchronize()
+            c.check(sample_ids(c.batch, 32, 16))
+            C = c.views()[2].cpu().numpy()
+            mask = np.ones(C.shape, bool)
+            for b in range(c.batch):
+                for j in range(c.N):
+                    o = b * c.sC + j * c.ldc
+                    mask[o:o + c.M] = False
+            assert np.isnan(C[mask]).all(), tr
+    finally:
+        _force()
+
+
+def test_ksg_default_plans_and_small_batches():
+    """The default plan picks ksg for the large config-2 shapes; batches
+    smaller than one unit per group, and batch 1, are exact too."""
+    for tr in ("NN", "NT", "TT"):
+        for batch in (1, 3, 150, 1201):
+            c = Case(F32, tr[0], tr[1], 80, 80, 80, batch, 8, -0.75, 1.25)
+            c.run()
+            torch.cuda.synchronize()
+            c.check()

@@ -142,19 +142,47 @@ def test_tn_extended_domain(dtype):
 
 
 # ---------------------------------------------------------------- full-size launch configs, sampled
-@pytest.mark.parametrize("n", [4, 16, 32, 64, 80])
-def test_config2_full_batch_sampled(n):
-    """The bench's launch configuration (config 2 full batch), checked on the
-    first/last 256 problems and 1024 seeded random ones."""
-    c = Case(F32, "N", "N", n, n, n, config2_batch(n), 1, 1.5, 0.5)
+@pytest.mark.parametrize("tr", ["NN", "NT", "TT"])
+@pytest.mark.parametrize("n", list(range(4, 81, 4)))
+def test_config2_full_batch_sampled(n, tr):
+    """The bench's launch configuration (config 2 full batch, the plan the
+    bench runs -- tuned table entry or cost model), checked on the first /
+    last 256 problems and 1024 seeded random ones."""
+    c = Case(F32, tr[0], tr[1], n, n, n, config2_batch(n), 1, 1.5, 0.5)
     c.run()
     c.check(sample_ids(c.batch))
 
 
-def test_config5_full_batch_sampled():
-    c = Case(F64, "N", "N", 32, 32, 32, 2_000_000, 4, 1.0, 0.0)
+@pytest.mark.parametrize("i", range(64))
+def test_config3_full_batch_sampled(i):
+    """Config 3 at its bench batch (100000 per shape), sampled."""
+    M, N, K = config3_shapes()[i]
+    c = Case(F32, "N", "N", M, N, K, 100000, 2, 1.0, 1.0)
     c.run()
     c.check(sample_ids(c.batch))
+
+
+@pytest.mark.parametrize("shape", config4_shapes())
+def test_config4_full_batch_sampled(shape):
+    """Config 4 (TN) at its bench batch (500000 per shape), sampled."""
+    M, N, K = shape
+    c = Case(F32, "T", "N", M, N, K, 500000, 3, -1.0, 0.25)
+    c.run()
+    c.check(sample_ids(c.batch))
+
+
+@pytest.mark.parametrize("tr", ["NN", "NT"])
+@pytest.mark.parametrize("n", [32, 80])
+def test_config5_full_batch_sampled(n, tr):
+    """Config 5 (fp64) at the bench's launch size: the full 2e6 batch where
+    it fits, else one bench chunk (60 % of HBM, bench.py)."""
+    per = 3 * n * n * 8
+    cap = int(0.60 * torch.cuda.get_device_properties(0).total_memory) // per
+    c = Case(F64, tr[0], tr[1], n, n, n, min(2_000_000, cap), 4, 1.0, 0.0)
+    c.run()
+    c.check(sample_ids(c.batch))
+    del c
+    torch.cuda.empty_cache()
 
 
 # ---------------------------------------------------------------- exactness / invariants
