@@ -12,9 +12,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <vector>
 
 #include "../../include/iaat.h"
 #include "iaat_device.cuh"
@@ -56,7 +58,9 @@ struct KeyHash {
 };
 
 std::mutex g_mu;
-std::unordered_map<Key, Plan, KeyHash> g_cache;
+// Plans are immutable once built and shared: a caller keeps its plan alive
+// through the shared_ptr even if another thread evicts the cache meanwhile.
+std::unordered_map<Key, std::shared_ptr<const Plan>, KeyHash> g_cache;
 
 Key make_key(const PlanRequest &r)
 {
@@ -100,15 +104,19 @@ int64_t forced_key()
     return (int64_t)h;
 }
 
-const Plan &cached_plan(const PlanRequest &r)
+std::shared_ptr<const Plan> cached_plan(const PlanRequest &r)
 {
     Key k = make_key(r);
     k.v[18] = forced_key();
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        auto it = g_cache.find(k);
+        if (it != g_cache.end()) return it->second;
+    }
+    auto plan = std::make_shared<const Plan>(make_plan(r));  // planned outside the lock
     std::lock_guard<std::mutex> lock(g_mu);
-    auto it = g_cache.find(k);
-    if (it != g_cache.end()) return it->second;
-    if (g_cache.size() > 4096) g_cache.clear();
-    return g_cache.emplace(k, make_plan(r)).first->second;
+    if (g_cache.size() > 4096) g_cache.clear();  // holders keep their plans alive
+    return g_cache.emplace(k, plan).first->second;
 }
 
 struct DevInfo {
@@ -249,11 +257,27 @@ iaat_status_t launch_scale(iaat_dtype_t dt, char *C, void *const *Carr, int64_t 
     return IAAT_SUCCESS;
 }
 
-iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t N, int64_t K,
-                  const void *alpha, const void *A, int64_t lda, int64_t sA, const void *B, int64_t ldb,
-                  int64_t sB, const void *beta, void *C, int64_t ldc, int64_t sC, int64_t batch,
-                  const void *const *Aarr, const void *const *Barr, void *const *Carr, bool ptr_array,
-                  void *stream)
+// One call, validated and planned but not yet enqueued (row a1 + a2): the
+// grouped API prepares every group before it launches any.
+struct Prepared {
+    int kind = 0;  // 0: nothing to do (quick return), 1: C = beta*C, 2: GEMM plan
+    iaat_dtype_t dt = IAAT_R32F;
+    int ta = 0, tb = 0, elt = 4, sm_count = 0;
+    int64_t M = 0, N = 0, K = 0, ldc = 0, sC = 0, batch = 0;
+    double a = 0, b = 0, ai = 0, bi = 0;
+    const void *A = nullptr, *B = nullptr;
+    void *C = nullptr;
+    const void *const *Aarr = nullptr;
+    const void *const *Barr = nullptr;
+    void *const *Carr = nullptr;
+    std::shared_ptr<const Plan> plan;
+};
+
+iaat_status_t prepare(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t N, int64_t K,
+                      const void *alpha, const void *A, int64_t lda, int64_t sA, const void *B, int64_t ldb,
+                      int64_t sB, const void *beta, void *C, int64_t ldc, int64_t sC, int64_t batch,
+                      const void *const *Aarr, const void *const *Barr, void *const *Carr, bool ptr_array,
+                      Prepared &out)
 {
     const int ta = parse_op(transA), tb = parse_op(transB);
     iaat_status_t st = validate(dt, ta, tb, M, N, K, lda, ldb, ldc, batch, alpha, beta);
@@ -262,6 +286,7 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
     if (!ptr_array && (sA < 0 || sB < 0 || sC < 0)) return IAAT_ERROR_INVALID_VALUE;
     // C problems must not overlap (reading A18)
     if (!ptr_array && batch > 1 && M > 0 && N > 0 && sC < (N - 1) * ldc + M) return IAAT_ERROR_INVALID_VALUE;
+    out = Prepared();
     if (M == 0 || N == 0 || batch == 0) return IAAT_SUCCESS;  // nothing to do (reading A5)
     const double a = scalar(dt, alpha), b = scalar(dt, beta);
     const double ai = scalar_im(dt, alpha), bi = scalar_im(dt, beta);
@@ -277,10 +302,31 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
     DevInfo dev;
     st = device_info(dev);
     if (st != IAAT_SUCCESS) return st;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (no_ab)
-        return launch_scale(dt, static_cast<char *>(C), Carr, sC, M, N, ldc, batch, b, bi, s, dev.sm_count);
-
+    out.dt = dt;
+    out.ta = ta;
+    out.tb = tb;
+    out.elt = elt;
+    out.sm_count = dev.sm_count;
+    out.M = M;
+    out.N = N;
+    out.K = K;
+    out.ldc = ldc;
+    out.sC = sC;
+    out.batch = batch;
+    out.a = a;
+    out.b = b;
+    out.ai = ai;
+    out.bi = bi;
+    out.A = A;
+    out.B = B;
+    out.C = C;
+    out.Aarr = Aarr;
+    out.Barr = Barr;
+    out.Carr = Carr;
+    if (no_ab) {
+        out.kind = 1;
+        return IAAT_SUCCESS;
+    }
     PlanRequest r;
     r.dtype = (int)dt;
     r.transA = ta;
@@ -304,9 +350,29 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
     r.align = ptr_array ? elt : align;
     r.sm_count = dev.sm_count;
     r.ptr_array = ptr_array ? 1 : 0;
-    const Plan &plan = cached_plan(r);
-    if (plan.status != 0) return (iaat_status_t)plan.status;
+    out.plan = cached_plan(r);
+    if (out.plan->status != 0) return (iaat_status_t)out.plan->status;
+    out.kind = 2;
+    return IAAT_SUCCESS;
+}
 
+iaat_status_t launch(const Prepared &pr, cudaStream_t s)
+{
+    if (pr.kind == 0) return IAAT_SUCCESS;
+    if (pr.kind == 1)
+        return launch_scale(pr.dt, static_cast<char *>(pr.C), pr.Carr, pr.sC, pr.M, pr.N, pr.ldc, pr.batch, pr.b,
+                            pr.bi, s, pr.sm_count);
+    const Plan &plan = *pr.plan;
+    const int elt = pr.elt, ta = pr.ta, tb = pr.tb;
+    const double a = pr.a, b = pr.b, ai = pr.ai, bi = pr.bi;
+    const void *A = pr.A, *B = pr.B;
+    void *C = pr.C;
+    const void *const *Aarr = pr.Aarr;
+    const void *const *Barr = pr.Barr;
+    void *const *Carr = pr.Carr;
+    struct {
+        int dtype;
+    } r{(int)pr.dt};
     if (plan.ksg) {
         IaatKsgParams kp = plan.kgp;
         kp.alpha = a;
@@ -327,8 +393,12 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
     }
     if (plan.ks) {
         IaatKsParams kp = plan.ksp;
+#ifdef IAAT_EXPERIMENTS
         static const int ks_debug = std::getenv("IAAT_DEBUG_KS") ? std::atoi(std::getenv("IAAT_DEBUG_KS")) : 0;
         kp.debug = ks_debug;
+#else
+        kp.debug = 0;
+#endif
         kp.alpha_i = ai;
         kp.beta_i = bi;
         kp.C = static_cast<char *>(C);
@@ -387,7 +457,11 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
     kp.alpha_i = ai;
     kp.beta_i = bi;
     LaunchFn fn = kLaunch[r.dtype][ta * 2 + tb][plan.vec];
+#ifdef IAAT_EXPERIMENTS
     static const int smem_pad = std::getenv("IAAT_DEBUG_SMEM_PAD") ? std::atoi(std::getenv("IAAT_DEBUG_SMEM_PAD")) : 0;
+#else
+    constexpr int smem_pad = 0;
+#endif
     cudaError_t e = fn(kp, plan.grid, plan.block, std::min(plan.smem + smem_pad, IAAT_SMEM_LIMIT), s);
     if (e != cudaSuccess) {
         g_last_cuda_error = (int)e;
@@ -395,6 +469,20 @@ iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t 
     }
     g_launches.fetch_add(1);
     return IAAT_SUCCESS;
+}
+
+
+iaat_status_t run(iaat_dtype_t dt, char transA, char transB, int64_t M, int64_t N, int64_t K,
+                  const void *alpha, const void *A, int64_t lda, int64_t sA, const void *B, int64_t ldb,
+                  int64_t sB, const void *beta, void *C, int64_t ldc, int64_t sC, int64_t batch,
+                  const void *const *Aarr, const void *const *Barr, void *const *Carr, bool ptr_array,
+                  void *stream)
+{
+    Prepared pr;
+    iaat_status_t st = prepare(dt, transA, transB, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC, batch,
+                               Aarr, Barr, Carr, ptr_array, pr);
+    if (st != IAAT_SUCCESS) return st;
+    return launch(pr, static_cast<cudaStream_t>(stream));
 }
 
 }  // namespace
@@ -575,11 +663,18 @@ iaat_status_t iaat_gemm_grouped_strided(iaat_dtype_t dtype, int64_t group_count,
             return IAAT_ERROR_INVALID_VALUE;
         if (M[g] > 0 && N[g] > 0 && batch[g] > 0 && !C[g]) return IAAT_ERROR_INVALID_VALUE;
     }
+    // validate and plan every group (pointers, alignment, device, planner
+    // status) before enqueueing any: an argument error leaves every C untouched
+    std::vector<Prepared> prep((size_t)group_count);
     for (int64_t g = 0; g < group_count; ++g) {
-        iaat_status_t st = run(dtype, transA[g], transB[g], M[g], N[g], K[g], al + g * ns * es, A[g], lda[g],
-                               strideA[g], B[g], ldb[g], strideB[g], be + g * ns * es, C[g], ldc[g], strideC[g],
-                               batch[g], nullptr, nullptr, nullptr, false, stream);
-        if (st != IAAT_SUCCESS) return st;  // only device-side (CUDA) errors can remain here
+        iaat_status_t st = prepare(dtype, transA[g], transB[g], M[g], N[g], K[g], al + g * ns * es, A[g], lda[g],
+                                   strideA[g], B[g], ldb[g], strideB[g], be + g * ns * es, C[g], ldc[g],
+                                   strideC[g], batch[g], nullptr, nullptr, nullptr, false, prep[(size_t)g]);
+        if (st != IAAT_SUCCESS) return st;
+    }
+    for (int64_t g = 0; g < group_count; ++g) {
+        iaat_status_t st = launch(prep[(size_t)g], static_cast<cudaStream_t>(stream));
+        if (st != IAAT_SUCCESS) return st;  // launch (CUDA) errors only: arguments were all checked above
     }
     return IAAT_SUCCESS;
 }

@@ -35,6 +35,15 @@
 #include "iaat_device.cuh"
 #include "iaat_params.h"
 
+// Measurement-only timing modes (IAAT_DEBUG_KS): compiled
+// only into experiment builds (-DIAAT_EXPERIMENTS); the shipped library has
+// none of them, so no environment setting can make it skip work.
+#ifdef IAAT_EXPERIMENTS
+#define IAAT_KS_DEBUG(p) ((p).debug)
+#else
+#define IAAT_KS_DEBUG(p) 0
+#endif
+
 namespace iaat {
 
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2,
@@ -180,7 +189,9 @@ __device__ void ks_producer(const IaatKsParams &p, const CUtensorMap *tmA, const
             bulk_prefetch_l2(reinterpret_cast<const void *>(lo), (uint32_t)(hi - lo));
         }
         for (int c = 0; c < p.nchunks; ++c, ++it) {
+#ifdef IAAT_EXPERIMENTS
             if (it >= p.S && (p.debug & 4)) return;  // timing mode: fill the ring once, never refill
+#endif
             if (it >= p.S) mbar_wait(&empty[s], phase);
             unsigned char *st = ring + (size_t)s * p.stage_bytes;
             mbar_arrive_expect_tx(&full[s], tx);
@@ -379,7 +390,8 @@ __device__ __forceinline__ void ks_fma_class_loop(const IaatKsParams &p, const I
     // p and c arrive as generic pointers, and a load through them after a
     // store to C could not be hoisted by the compiler.
     const int K = p.K, kc = p.kc, nchunks = p.nchunks, P = p.P, S = p.S, M = p.M, N = p.N, ldc = p.ldc;
-    const int stage_bytes = p.stage_bytes, a_bytes = p.a_bytes, dbg = p.debug;
+    const int stage_bytes = p.stage_bytes, a_bytes = p.a_bytes;
+    const int dbg = IAAT_KS_DEBUG(p);
     const bool beta_zero = p.beta_zero != 0, c_vec = p.c_vec != 0;
     const int64_t nunits = p.nunits, batch = p.batch;
     char *const Cbase = p.C;
@@ -517,7 +529,8 @@ __device__ __forceinline__ void ks_dmma_class_loop(const IaatKsParams &p, const 
 {
     constexpr bool AK = TA, BK = !TB;
     const int K = p.K, kc = p.kc, nchunks = p.nchunks, P = p.P, S = p.S, M = p.M, N = p.N, ldc = p.ldc;
-    const int stage_bytes = p.stage_bytes, a_bytes = p.a_bytes, dbg = p.debug;
+    const int stage_bytes = p.stage_bytes, a_bytes = p.a_bytes;
+    const int dbg = IAAT_KS_DEBUG(p);
     const bool beta_zero = p.beta_zero != 0, c_vec = p.c_vec != 0;
     const int64_t nunits = p.nunits, batch = p.batch;
     const int g = lane >> 2, t = lane & 3;

@@ -385,36 +385,46 @@ __device__ __forceinline__ void ksg_producer(const IaatKsgParams &p, const CUten
     int s = 0, it = 0;
     uint32_t phase = 0, rphase = 0;
     int prev_b0 = -1;
+    auto issue_chunk = [&](int b0, int c) {
+        if (it >= p.S) bar_wait(sm.empty + 8 * s, phase);
+        const uint32_t st = sm.ring + (uint32_t)(s * p.stage_bytes), fb = sm.full + 8 * s;
+        bar_expect_tx(fb, tx);
+        const int k0 = c * KC;
+        if (TA) tma_load_3d(st, tmA, k0, 0, b0, fb, pol);
+        else tma_load_3d(st, tmA, 0, k0, b0, fb, pol);
+        if (TB) tma_load_3d(st + p.a_bytes, tmB, 0, k0, b0, fb, pol);
+        else tma_load_3d(st + p.a_bytes, tmB, k0, 0, b0, fb, pol);
+        if (++s == p.S) {
+            s = 0;
+            if (it >= 2 * p.S - 1) phase ^= 1u;
+        }
+        ++it;
+    };
+    const int nch = (DBG & 1) ? 0 : p.nchunks;
     for (int64_t u = (int64_t)blockIdx.x * G + g; u < p.nunits; u += (int64_t)gridDim.x * G) {
         const int b0 = (int)(u * p.P);
-        for (int c = 0; c < ((DBG & 1) ? 0 : p.nchunks); ++c, ++it) {
-            if (it >= p.S) bar_wait(sm.empty + 8 * s, phase);
-            const uint32_t st = sm.ring + (uint32_t)(s * p.stage_bytes), fb = sm.full + 8 * s;
-            bar_expect_tx(fb, tx);
-            const int k0 = c * KC;
-            if (TA) tma_load_3d(st, tmA, k0, 0, b0, fb, pol);
-            else tma_load_3d(st, tmA, 0, k0, b0, fb, pol);
-            if (TB) tma_load_3d(st + p.a_bytes, tmB, 0, k0, b0, fb, pol);
-            else tma_load_3d(st + p.a_bytes, tmB, k0, 0, b0, fb, pol);
-            if (++s == p.S) {
-                s = 0;
-                if (it >= 2 * p.S - 1) phase ^= 1u;
+        // the first ring's worth of this unit's chunks (their slots free up
+        // as the previous unit's k loop ends), then the previous unit's C
+        // (stored as soon as its epilogue is done) and this unit's C_in --
+        // early, so that both overlap this unit's k loop -- then the rest
+        int c = 0;
+        for (; c < min(p.S, nch); ++c) issue_chunk(b0, c);
+        if (!(DBG & 2)) {
+            if (prev_b0 >= 0) {
+                bar_wait(sm.cready, rphase);
+                rphase ^= 1u;
+                tma_store_3d(tmC, sm.cbuf, 0, 0, prev_b0);
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             }
+            if (!p.beta_zero) {
+                bar_expect_tx(sm.cfull, (uint32_t)p.c_tx);
+                tma_load_3d(sm.cbuf, tmC, 0, 0, b0, sm.cfull, pol);
+            } else {
+                bar_arrive(sm.cfull);
+            }
+            prev_b0 = b0;
         }
-        if (DBG & 2) continue;
-        if (prev_b0 >= 0) {
-            bar_wait(sm.cready, rphase);
-            rphase ^= 1u;
-            tma_store_3d(tmC, sm.cbuf, 0, 0, prev_b0);
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        }
-        if (!p.beta_zero) {
-            bar_expect_tx(sm.cfull, (uint32_t)p.c_tx);
-            tma_load_3d(sm.cbuf, tmC, 0, 0, b0, sm.cfull, pol);
-        } else {
-            bar_arrive(sm.cfull);
-        }
-        prev_b0 = b0;
+        for (; c < nch; ++c) issue_chunk(b0, c);
     }
     if (prev_b0 >= 0 && !(DBG & 2)) {
         bar_wait(sm.cready, rphase);
@@ -423,20 +433,21 @@ __device__ __forceinline__ void ksg_producer(const IaatKsgParams &p, const CUten
     }
 }
 
-// The kernel body: 12 warps = three warpgroups.  Warpgroup 0 holds the
-// producers (warp g < G serves group g; the others retire at once) and
-// gives registers back (setmaxnreg.dec); warpgroups 1-2 are the G*W = 8
-// consumer warps, which take them (setmaxnreg.inc) for the big register
-// tiles.  Consumer c = warp - 4 is warp c % W of group c / W, so every SMSP
-// (warp % 4) hosts warps of two different groups.
-#define IAAT_KSG_THREADS IAAT_KSG_THREADS_HOST
+// The kernel body: 1 + G*W/4 warpgroups.  Warpgroup 0 holds the producers
+// (warp g < G serves group g; the others retire at once) and gives
+// registers back (setmaxnreg.dec); the G*W = 8 or 12 consumer warps take
+// them (setmaxnreg.inc) for the register tiles.  Consumer c = warp - 4 is
+// warp c % W of group c / W, so every SMSP (warp % 4) hosts warps of
+// different groups.
+#define IAAT_KSG_THREADS_OF(GW) (128 + 32 * (GW))
 #define IAAT_KSG_PRODUCER_REGS 40
-#define IAAT_KSG_CONSUMER_REGS 232
+#define IAAT_KSG_CONSUMER_REGS_OF(GW) ((GW) == 8 ? 232 : 152)
 template <bool TA, bool TB, int MR, int NR, int LR, int KC, int KU, int G, int W, int DBG = 0>
 __device__ __forceinline__ void ksg_body(const IaatKsgParams &p, const CUtensorMap *tmA, const CUtensorMap *tmB,
                                          const CUtensorMap *tmC)
 {
-    static_assert(G * W == 8, "ksg: two warpgroups of consumers");
+    static_assert(G * W == 8 || G * W == 12, "ksg: two or three warpgroups of consumers");
+    static_assert(G <= IAAT_KSG_MAX_GROUPS, "ksg: barrier area holds IAAT_KSG_MAX_GROUPS groups");
     extern __shared__ __align__(1024) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x < G) {
@@ -456,7 +467,7 @@ __device__ __forceinline__ void ksg_body(const IaatKsgParams &p, const CUtensorM
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(IAAT_KSG_PRODUCER_REGS));
         if (warp < G) ksg_producer<TA, TB, KC, G, DBG>(p, tmA, tmB, tmC, smem, warp, lane);
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(IAAT_KSG_CONSUMER_REGS));
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(IAAT_KSG_CONSUMER_REGS_OF(G * W)));
         const int c = warp - 4;
         ksg_consumer<TA, TB, MR, NR, LR, KC, KU, G, W, DBG>(p, smem, c / W, c % W, lane);
     }

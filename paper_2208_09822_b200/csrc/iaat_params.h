@@ -85,6 +85,11 @@ struct IaatKParams {
 // S-stage ring of TMA boxes.  The two CUtensorMaps travel as separate
 // __grid_constant__ kernel parameters.
 #define IAAT_KS_MAX_STAGES 12
+// fp64 / ZGEMM DMMA warp tiles of 10 or more 8x8 blocks keep their
+// accumulators without spills only above 128 registers per thread: their
+// kernels are compiled for at most 384 threads (168 registers) and the
+// planner sizes their CTAs accordingly (spill-free catalog).
+#define IAAT_KSD_THREADS(wm, wn) ((wm) * (wn) >= 10 ? 384 : IAAT_MAX_THREADS)
 #define IAAT_KS_BAR_BYTES 256   // mbarriers; the stage ring starts at the next 1024 B boundary
 
 struct IaatKsParams {
@@ -128,7 +133,6 @@ struct IaatKsParams {
 #define IAAT_KSG_MAX_GROUPS 4
 #define IAAT_KSG_GROUP_BARS (2 * IAAT_KSG_MAX_STAGES + 2)  // full[S], empty[S], cfull, cready
 #define IAAT_KSG_BAR_BYTES 1024
-#define IAAT_KSG_THREADS_HOST 384  // == IAAT_KSG_THREADS (iaat_ksg.cuh): 3 warpgroups
 
 struct IaatKsgParams {
     int64_t batch;

@@ -575,9 +575,12 @@ bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
     pl.vec = 1;
     pl.ctas = 1;
     pl.grid = (int)std::min<int64_t>((k.nunits + e.g - 1) / e.g, (int64_t)r.sm_count);
-    pl.block = IAAT_KSG_THREADS_HOST;
+    pl.block = 128 + 32 * e.g * e.w;  // IAAT_KSG_THREADS_OF(g * w): producer warpgroup + consumers
     pl.smem = IAAT_KSG_BAR_BYTES + 1024 + e.g * k.group_bytes;
     pl.est_total = best.cost;
+    // the paper's cost over the Mv x Nv tiling: smem words
+    // the lanes' tiles read per k-step, plus the C traffic
+    pl.memops = (int64_t)(best.Mv / e.mr) * (best.Nv / e.nr) * (e.mr + e.nr) * K + 2 * M * N;
     pl.status = 0;
     out = pl;
     return true;
@@ -1077,7 +1080,7 @@ bool plan_ks_zdmma(const PlanRequest &r, const Knobs &kn, Plan &out)
             const int tm = (int)(M / (8 * wm)), tn = (int)(N / (8 * wn)), tiles = tm * tn;
             for (int ctas = 1; ctas <= 3; ++ctas) {
                 if (kn.ctas && ctas != kn.ctas) continue;
-                const int wmax = std::min(IAAT_MAX_THREADS / 32, 16 / ctas) - 1;
+                const int wmax = std::min(IAAT_KSD_THREADS(wm, wn) / 32, 16 / ctas) - 1;
                 const int smem_cta = (int)std::min<int64_t>(IAAT_SMEM_LIMIT, 228 * 1024 / ctas - 1024);
                 for (int P = 1; P * tiles <= wmax; ++P) {
                     if (kn.p && P != kn.p) continue;
@@ -1384,7 +1387,7 @@ bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out)
                 const int tm = (int)(M / (8 * wm)), tn = (int)(N / (8 * wn)), tiles = tm * tn;
                 for (int ctas = 1; ctas <= 3; ++ctas) {
                     if (kn.ctas && ctas != kn.ctas) continue;
-                    const int wmax = IAAT_MAX_THREADS / 32 / ctas - 1;
+                    const int wmax = IAAT_KSD_THREADS(wm, wn) / 32 / ctas - 1;
                     const int smem_cta = (int)std::min<int64_t>(IAAT_SMEM_LIMIT, 228 * 1024 / ctas - 1024);
                     for (int P = 1; P * tiles <= wmax; ++P) {
                         if (kn.p && P != kn.p) continue;
@@ -1531,9 +1534,10 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
         const IaatKsgCatalogEntry &e = kKsgCatalog[p.kg_entry];
         add("\"family\": \"ksg\", \"entry\": %d, \"mr\": %d, \"nr\": %d, \"lane_rows\": %d, \"kc\": %d, "
             "\"ku\": %d, \"groups\": %d, \"warps_per_group\": %d, \"Mv\": %d, \"Nv\": %d, \"P\": %d, \"S\": %d, "
-            "\"c_pitch\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, \"nunits\": %lld, \"est\": %.0f, ",
+            "\"c_pitch\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, \"nunits\": %lld, \"est\": %.0f, "
+            "\"memops\": %lld, ",
             p.kg_entry, e.mr, e.nr, e.lr, e.kc, e.ku, e.g, e.w, q.Mv, q.Nv, q.P, q.S, q.c_pitch, p.grid, p.block,
-            p.smem, (long long)q.nunits, p.est_total);
+            p.smem, (long long)q.nunits, p.est_total, (long long)p.memops);
         s += "\"classes\": []}";
         return s;
     }

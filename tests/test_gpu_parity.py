@@ -591,3 +591,34 @@ def test_grouped_variable_size_batches(dtype):
     for c, r in zip(cases, ref_C):
         c.check()
         assert bits_equal(c.views()[2], r.views()[2])
+
+
+def test_grouped_argument_errors_enqueue_nothing():
+    """Every group is validated and planned before any is enqueued: a NULL A
+    or a misaligned base in the LAST group fails the call and leaves the C of
+    every earlier group untouched (include/iaat.h, grouped API)."""
+    from paper_2208_09822_b200 import iaat
+    cases = [Case(F32, "N", "N", 16, 16, 16, 200, 3, 1.0, 0.5), Case(F32, "N", "T", 40, 40, 40, 100, 4, 1.0, 0.5),
+             Case(F32, "T", "T", 9, 7, 5, 50, 5, 1.0, 0.5)]
+    before = [c.views()[2].clone() for c in cases]
+
+    def groups(bad):
+        gs = []
+        for i, c in enumerate(cases):
+            A, B, C = c.views()
+            a_ptr = A.data_ptr()
+            if i == len(cases) - 1 and bad == "null":
+                a_ptr = 0
+            if i == len(cases) - 1 and bad == "misaligned":
+                a_ptr += 2  # not element-aligned
+            gs.append(dict(transA=c.tA, transB=c.tB, M=c.M, N=c.N, K=c.K, alpha=c.alpha, A=a_ptr, lda=c.lda,
+                           strideA=c.sA, B=B.data_ptr(), ldb=c.ldb, strideB=c.sB, beta=c.beta, C=C.data_ptr(),
+                           ldc=c.ldc, strideC=c.sC, batch=c.batch))
+        return gs
+
+    for bad in ("null", "misaligned"):
+        st = iaat.iaat_gemm_grouped_strided(0, groups(bad), torch.cuda.current_stream().cuda_stream)
+        assert st == 1, (bad, st)  # IAAT_ERROR_INVALID_VALUE
+        torch.cuda.synchronize()
+        for c, b0 in zip(cases, before):
+            assert bits_equal(c.views()[2], b0), bad

@@ -36,8 +36,33 @@ def plan(dt, tr, M, N, K, batch=10000, beta0=False, align=256, pad=0):
                                    beta0, False, align, 148)
 
 
+KSG = {e["index"]: e for e in CAT if e["family"] == "ksg"}
+
+
+def check_ksg_plan(p, tr, M, N):
+    """ksg (csrc/iaat_ksg.cuh): one lane-grid class whose warp blocks tile the
+    Mv x Nv problem exactly; Mv - M, Nv - N < one warp block (the copy
+    engine's zero fill covers them, the TMA store clips them), whole
+    problems per group, M on a 16-byte C granule, smem within the limit."""
+    e = KSG[p["entry"]]
+    assert e["trans"] == tr and (e["mr"], e["nr"], e["lr"]) == (p["mr"], p["nr"], p["lane_rows"])
+    br, bc = e["lr"] * e["mr"], (32 // e["lr"]) * e["nr"]
+    assert p["Mv"] % br == 0 and p["Nv"] % bc == 0
+    assert M <= p["Mv"] < M + br and N <= p["Nv"] < N + bc
+    assert M % 4 == 0
+    wpp = (p["Mv"] // br) * (p["Nv"] // bc)
+    assert wpp * p["P"] == e["w"]
+    assert e["g"] * e["w"] in (8, 12) and p["block"] == 128 + 32 * e["g"] * e["w"]
+    assert 1 <= p["S"] <= 8 and p["c_pitch"] >= p["Mv"] and p["c_pitch"] % 4 == 0
+    assert p["smem"] <= 227 * 1024
+    assert p["grid"] <= 148
+
+
 def check_plan(p, dt, tr, M, N):
     assert p["status"] == 0, p
+    if p.get("family") == "ksg":
+        check_ksg_plan(p, tr, M, N)
+        return
     cover = np.zeros((M, N), dtype=np.int32)
     dname = "f32" if dt == 0 else "f64"
     vw = 4 if dt == 0 else 2
@@ -139,7 +164,10 @@ def test_memops_is_paper_cost():
     """memops = sum over tiles (m_i + n_i) K + 2MN."""
     for (M, N, K) in [(15, 15, 15), (64, 64, 64), (7, 80, 3)]:
         p = plan(0, "NN", M, N, K)
-        s = sum(c["tiles"] * (c["mr"] + c["nr"]) for c in p["classes"])
+        if p["family"] == "ksg":  # lane tiles over the Mv x Nv tiling
+            s = (p["Mv"] // p["mr"]) * (p["Nv"] // p["nr"]) * (p["mr"] + p["nr"])
+        else:
+            s = sum(c["tiles"] * (c["mr"] + c["nr"]) for c in p["classes"])
         assert p["memops"] == s * K + 2 * M * N
 
 
@@ -161,7 +189,14 @@ def test_catalog_register_budget():
             assert gen.fma_regs(e["dtype"], e["trans"], e["mr"], e["nr"]) <= gen.REG_BUDGET[e["dtype"]]
             assert 1 <= e["mr"] <= 8 and 1 <= e["nr"] <= 8
         elif e["family"] == "ksu_fma":
-            assert e["dtype"] == "f32" and (e["mr"], e["nr"]) in gen.KSU_TILES
+            assert e["dtype"] == "f32" and (e["mr"], e["nr"]) in gen.ksu_tiles(e["trans"])
+        elif e["family"] == "ksg":
+            # lane-grid register tiles (csrc/iaat_ksg.cuh): at most 128
+            # accumulators, lanes lr x 32/lr, two or three consumer warpgroups
+            assert e["dtype"] == "f32" and e["trans"] != "TN"
+            assert e["mr"] * e["nr"] <= 128 and 32 % e["lr"] == 0
+            assert e["g"] * e["w"] in (8, 12) and e["g"] <= 4 and e["kc"] in (16, 32) and e["ku"] in (2, 4)
+            assert tuple(e[k] for k in ("trans", "mr", "nr", "lr", "kc", "ku", "g", "w")) == gen.KSG_TILES[e["index"]]
         elif e["family"] == "ks_dmma" and e["dtype"] == "c64":
             assert (e["mr"] // 8, e["nr"] // 8) in gen.KSZ_TILES
         elif e["family"] in ("ks_fma", "ks1_fma"):

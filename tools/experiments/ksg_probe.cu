@@ -28,7 +28,7 @@
     } while (0)
 
 template <bool TA, bool TB, int MR, int NR, int LR, int KC, int KU, int G, int W, int DBG>
-__global__ void __launch_bounds__(IAAT_KSG_THREADS, 1)
+__global__ void __launch_bounds__(IAAT_KSG_THREADS_OF(G * W), 1)
     kprobe(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmC, const __grid_constant__ IaatKsgParams p)
 {
@@ -204,7 +204,7 @@ static void run(const Variant &v, int sms, float *dA, float *dB, float *dC, floa
         return;
     }
     CK(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int threads = IAAT_KSG_THREADS;
+    const int threads = IAAT_KSG_THREADS_OF(v.G * v.W);
     const size_t csz = (size_t)batch * M * N * 4;
     CK(cudaMemcpy(dC, dC0, csz, cudaMemcpyDeviceToDevice));
     void *args[4] = {&tA, &tB, &tC, &p};
@@ -251,21 +251,17 @@ int main(int argc, char **argv)
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     std::vector<Variant> vs = {
         V("NN80_10x10_l4_k16u2_g4w2_p1_s2", false, false, 80, 80, 10, 10, 4, 16, 2, 4, 2, 1, 2),
+        VD("NN80_10x10_l4_k16u2_g4w2_p1_s2_d1", false, false, 80, 80, 10, 10, 4, 16, 2, 4, 2, 1, 2, 1),
+        VD("NN80_10x10_l4_k16u2_g4w2_p1_s2_d2", false, false, 80, 80, 10, 10, 4, 16, 2, 4, 2, 1, 2, 2),
         VD("NN80_10x10_l4_k16u2_g4w2_p1_s2_d3", false, false, 80, 80, 10, 10, 4, 16, 2, 4, 2, 1, 2, 3),
-        V("NN80_10x10_l4_k16u4_g4w2_p1_s2", false, false, 80, 80, 10, 10, 4, 16, 4, 4, 2, 1, 2),
-        VD("NN80_10x10_l4_k16u4_g4w2_p1_s2_d3", false, false, 80, 80, 10, 10, 4, 16, 4, 4, 2, 1, 2, 3),
-        V("NN80_10x5_l4_k32u4_g2w4_p1_s3", false, false, 80, 80, 10, 5, 4, 32, 4, 2, 4, 1, 3),
-        VD("NN80_10x5_l4_k32u4_g2w4_p1_s3_d3", false, false, 80, 80, 10, 5, 4, 32, 4, 2, 4, 1, 3, 3),
-        V("NN80_10x5_l4_k32u2_g2w4_p1_s3", false, false, 80, 80, 10, 5, 4, 32, 2, 2, 4, 1, 3),
-        V("NT80_10x10_l4_k16u2_g2w4_p2_s2", false, true, 80, 80, 10, 10, 4, 16, 2, 2, 4, 2, 2),
+        V("NN80_10x10_l4_k16u2_g2w4_p2_s2", false, false, 80, 80, 10, 10, 4, 16, 2, 2, 4, 2, 2),
+        V("NN80_10x5_l4_k32u4_g3w4_p1_s2", false, false, 80, 80, 10, 5, 4, 32, 4, 3, 4, 1, 2),
+        V("NN80_10x5_l4_k16u4_g3w4_p1_s3", false, false, 80, 80, 10, 5, 4, 16, 4, 3, 4, 1, 3),
+        V("NT80_10x10_l4_k16u2_g4w2_p1_s2", false, true, 80, 80, 10, 10, 4, 16, 2, 4, 2, 1, 2),
         V("TT80_10x10_l8_k16u2_g2w4_p2_s2", true, true, 80, 80, 10, 10, 8, 16, 2, 2, 4, 2, 2),
         V("NN64_8x8_l4_k32u4_g2w4_p2_s2", false, false, 64, 64, 8, 8, 4, 32, 4, 2, 4, 2, 2),
-        VD("NN64_8x8_l4_k32u4_g2w4_p2_s2_d3", false, false, 64, 64, 8, 8, 4, 32, 4, 2, 4, 2, 2, 3),
-        V("NN64_8x8_l4_k32u2_g2w4_p2_s2", false, false, 64, 64, 8, 8, 4, 32, 2, 2, 4, 2, 2),
-        V("NN64_16x8_l4_k16u2_g4w2_p2_s1", false, false, 64, 64, 16, 8, 4, 16, 2, 4, 2, 2, 1),
-        VD("NN64_16x8_l4_k16u2_g4w2_p2_s1_d3", false, false, 64, 64, 16, 8, 4, 16, 2, 4, 2, 2, 1, 3),
-        V("NT64_8x8_l4_k32u4_g2w4_p2_s2", false, true, 64, 64, 8, 8, 4, 32, 4, 2, 4, 2, 2),
-        V("TT64_8x8_l8_k32u4_g2w4_p2_s2", true, true, 64, 64, 8, 8, 8, 32, 4, 2, 4, 2, 2),
+        V("NN72_6x9_l4_k16u2_g4w3_p1_s2", false, false, 72, 72, 6, 9, 4, 16, 2, 4, 3, 1, 2),
+        V("TT72_9x6_l8_k16u2_g4w3_p1_s2", true, true, 72, 72, 9, 6, 8, 16, 2, 4, 3, 1, 2),
     };
     size_t maxe = 0;
     for (auto &v : vs) {
