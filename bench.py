@@ -71,7 +71,7 @@ def roofline_of(s, cnt, t, pk):
                 "frac": round(s.flops(cnt) / t / 1e12 / cmp_peak, 4),
                 "peak_source": ("derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md)" if fp32 else
                                 "derived: 148 SM x 64 FP64 FMA/clk (DMMA) x 2 x 1.965 GHz (DESIGN.md)")}
-    roof["traffic"] = load_traffic(s.name())
+    roof["traffic"] = load_traffic(s.name(), cnt)
     return roof
 
 
@@ -141,7 +141,8 @@ def workload(cfg):
         for n in (8, 16, 32, 48, 64, 80):
             for tr in ("NN", "NT"):
                 S.append(Shape("f64", tr, n, n, n, 2_000_000, 1.0, 0.0, 4))
-        desc = "config5: fp64 NN/NT M=N=K in {8,16,32,48,64,80}, batch 2e6 (chunked to fit HBM), alpha=1, beta=0"
+        desc = ("config5: fp64 NN/NT M=N=K in {8,16,32,48,64,80}, global batch 2e6 sharded across the GPUs by "
+                "contiguous ranges (strong scaling), chunked to fit HBM, alpha=1, beta=0")
     elif cfg == 6:  # SURVEY f1 (not a BASELINE config): complex fp32, config-2 shape of sweep
         for n in range(4, 81, 4):
             b = (256 * 1024 * 1024) // (3 * n * n * 8)
@@ -172,6 +173,30 @@ def workload(cfg):
     else:
         raise SystemExit("unknown config %r" % cfg)
     return S, desc
+
+
+def plan_chunks(shapes, cfg, rank, world, hbm_cap):
+    """The calls one rank makes per step: (shape, first GLOBAL problem id,
+    count).  Config 5 is strong scaling (BASELINE.json: a fixed batch of
+    2,000,000 sharded across the GPUs by contiguous ranges): rank r owns
+    dist.shard_range(batch, r, world) and splits it into chunks that fit 60 %
+    of HBM.  Every other config is weak scaling: each rank runs the whole
+    workload on its own problems [r*batch, (r+1)*batch).  Inputs are
+    generated from the global ids, so a problem's data -- and its result --
+    do not depend on the split."""
+    from paper_2208_09822_b200.dist import shard_range
+    chunks = []
+    for s in shapes:
+        if cfg == 5:
+            lo, hi = shard_range(s.batch, rank, world)
+            ra, ca, rb, cb = s.stored()
+            per = (ra * ca + rb * cb + s.M * s.N) * s.elt
+            cnt = max(1, min(hi - lo, int(0.60 * hbm_cap) // per))
+            for c0 in range(lo, hi, cnt):
+                chunks.append((s, c0, min(cnt, hi - c0)))
+        else:
+            chunks.append((s, rank * s.batch, s.batch))
+    return chunks
 
 
 # ---------------------------------------------------------------- clocks
@@ -244,15 +269,7 @@ def run_ours(args, rank, world, local_rank):
     # --- allocate + fill (outside the timed region); one buffer set per (dtype, M,N,K)
     hbm_cap = torch.cuda.get_device_properties(dev).total_memory
     bufs = {}
-    chunks = []  # (shape, first_local, count) -- chunking for config 5
-    for s in shapes:
-        ra, ca, rb, cb = s.stored()
-        per = (ra * ca + rb * cb + s.M * s.N) * s.elt
-        cap = int(0.80 * hbm_cap) // (per * 2 if s.dtype == "f64" else per * 3)  # keep room for others
-        cnt = s.batch if args.config != 5 else min(s.batch, max(1, int(0.60 * hbm_cap) // per))
-        for lo in range(0, s.batch, cnt):
-            chunks.append((s, lo, min(cnt, s.batch - lo)))
-        _ = cap
+    chunks = plan_chunks(shapes, args.config, rank, world, hbm_cap)  # (shape, first global id, count)
     for s, lo, cnt in chunks:
         key = (s.dtype, s.M, s.N, s.K, s.tr, cnt)
         if key in bufs:
@@ -265,7 +282,7 @@ def run_ours(args, rank, world, local_rank):
         A = torch.empty(w * cnt * ra * ca, dtype=tdt[s.dtype], device=dev)
         B = torch.empty(w * cnt * rb * cb, dtype=tdt[s.dtype], device=dev)
         C = torch.empty(w * cnt * s.M * s.N, dtype=tdt[s.dtype], device=dev)
-        first = rank * s.batch + lo  # global problem ids: ranks own disjoint problems
+        first = lo  # global problem ids: ranks own disjoint problems
         datagen.fill_device(A, s.seed, datagen.MAT_A, w * ra, ca, w * ra, w * ra * ca, cnt, first)
         datagen.fill_device(B, s.seed, datagen.MAT_B, w * rb, cb, w * rb, w * rb * cb, cnt, first)
         datagen.fill_device(C, s.seed, datagen.MAT_C, w * s.M, s.N, w * s.M, w * s.M * s.N, cnt, first)
@@ -482,7 +499,7 @@ def run_chunked_config5(args, rank, world, local_rank, shapes, desc, chunks, buf
                          torch.empty(cnt * s.M * s.N, dtype=tdt, device=dev))
         A, B, C = bufs[key]
         ra, ca, rb, cb = s.stored()
-        first = rank * s.batch + lo
+        first = lo  # this rank's shard of the global batch (plan_chunks)
         datagen.fill_device(A, s.seed, datagen.MAT_A, ra, ca, ra, ra * ca, cnt, first)
         datagen.fill_device(B, s.seed, datagen.MAT_B, rb, cb, rb, rb * cb, cnt, first)
         for _ in range(args.warmup):
@@ -502,14 +519,16 @@ def run_chunked_config5(args, rank, world, local_rank, shapes, desc, chunks, buf
     clk = clocks.stop()
     total_ms = sum(v[0] for v in res.values())
     total_ms = allreduce_max(total_ms, world)
-    flops = sum(v[2].flops() for v in res.values())
-    value = flops * world / (total_ms * 1e-3) / 1e9
+    # strong scaling: the ranks share the fixed global batch; value = all
+    # ranks' flops over the slowest rank's GEMM time
+    flops = allreduce_sum(sum(v[2].flops(v[1]) for v in res.values()), world)
+    value = flops / (total_ms * 1e-3) / 1e9
     pk = peaks()
     shapes_out = []
     for nm, (ms, cnt, s) in res.items():
         t = ms * 1e-3
-        t_roof = max(s.flops() / (DMMA_PEAK_TFLOPS * 1e12), s.alg_bytes() / (pk["hbm_gbs"] * 1e9))
-        shapes_out.append({"shape": nm, "batch": cnt, "ms": round(ms, 4), "gflops": round(s.flops() / t / 1e9, 1),
+        t_roof = max(s.flops(cnt) / (DMMA_PEAK_TFLOPS * 1e12), s.alg_bytes(cnt) / (pk["hbm_gbs"] * 1e9))
+        shapes_out.append({"shape": nm, "batch": cnt, "ms": round(ms, 4), "gflops": round(s.flops(cnt) / t / 1e9, 1),
                            "frac_roofline": round(t_roof / t, 4)})
     nm, (ms, cnt, s) = max(res.items(), key=lambda kv: kv[1][0])
     dom_roof = roofline_of(s, cnt, ms * 1e-3, pk)
@@ -517,8 +536,12 @@ def run_chunked_config5(args, rank, world, local_rank, shapes, desc, chunks, buf
     dom_roof["share_of_step"] = round(ms / total_ms, 4)
     return {"metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total_ms, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc}, "roofline": dom_roof, "gpu_launches": int(n_launch), "clocks": clk,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "per_gpu": round(value / world, 1),
+            "config": {"workload": desc, "global_batch": shapes[0].batch,
+                       "parallelism": "dp%d: contiguous shards of the fixed global batch (dist.shard_range), "
+                                      "no collective on the data path" % world},
+            "roofline": dom_roof, "gpu_launches": int(n_launch), "clocks": clk,
             "shapes": shapes_out}
 
 
@@ -627,12 +650,50 @@ def run_oracle_timed(shapes, frac, repeats=1):
     return total_f / total_t / 1e9, threads, total_t
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_oracle_one_thread(shapes, frac):
+    """Per-core figure: the same oracle on ONE host thread, on a
+    small prefix of every shape's batch."""
+    import datagen
+    import oracle
+    dt = {"f32": np.float32, "f64": np.float64}
+    tt, ff = 0.0, 0.0
+    for s in shapes:
+        if s.cplx:
+            continue
+        n = max(1, int(s.batch * frac))
+        ra, ca, rb, cb = s.stored()
+        ids = np.arange(n)
+        A = datagen.fill_host(s.seed, 0, dt[s.dtype], ra, ca, ra, ra * ca, ids)
+        B = datagen.fill_host(s.seed, 1, dt[s.dtype], rb, cb, rb, rb * cb, ids)
+        C = datagen.fill_host(s.seed, 2, dt[s.dtype], s.M, s.N, s.M, s.M * s.N, ids)
+        t = time.perf_counter()
+        oracle.ref_gemm(s.tr[0], s.tr[1], s.M, s.N, s.K, s.alpha, A, ra, ra * ca, B, rb, rb * cb, s.beta, C,
+                        s.M, s.M * s.N, n, nthreads=1, want_den=False)
+        tt += time.perf_counter() - t
+        ff += s.flops(n)
+    return ff / tt / 1e9 if tt > 0 else None, frac
+
+
 def run_cpu_baseline(shapes, args):
     frac = args.cpu_frac
     gf, threads, t = run_oracle_timed(shapes, frac)
+    gf1, frac1 = run_oracle_one_thread(shapes, frac / 64)
     return {"value": round(gf, 3), "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+            "cpu_model": cpu_model(), "one_thread_gflops": round(gf1, 3) if gf1 else None,
             "sample": "first %.4g of every shape's batch of the same step (all %d calls), fp64-accumulating "
-                      "C triple loop, OpenMP over problems; %.1f s of CPU time" % (frac, len(shapes), t)}
+                      "C triple loop, OpenMP over problems; %.1f s of CPU time; one_thread: first %.4g on 1 thread"
+                      % (frac, len(shapes), t, frac1)}
 
 
 def run_reference_arm(args, rank, world):
@@ -697,13 +758,25 @@ def allreduce_max(x, world):
     return float(x)
 
 
-def load_traffic(name):
-    """dram bytes per launch from a committed ncu --set full capture, if any."""
+def allreduce_sum(x, world):
+    if world > 1 and _PG is not None:
+        import torch
+        dev = "cuda" if torch.cuda.is_available() and _PG.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+        _PG.all_reduce(t, op=_PG.ReduceOp.SUM)
+        return float(t.item())
+    return float(x)
+
+
+def load_traffic(name, batch):
+    """dram bytes per launch of exactly this launch (shape AND batch) from a
+    committed ncu --set full capture (profiles/traffic.json, key
+    "<shape>@<batch>"), else None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(name)
+        return d.get("%s@%d" % (name, batch))
     except Exception:
         return None
 
@@ -724,6 +797,10 @@ def main(argv=None):
     ap.add_argument("--grouped", action="store_true",
                     help="run the workload as one grouped (variable-size) call per step (SURVEY f4)")
     args = ap.parse_args(argv)
+    env_world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != env_world:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d: launch N>1 with "
+                         "torch.distributed.run --nproc-per-node N ... --gpus N" % (args.gpus, env_world))
     rank, world, local = init_dist()
     if args.impl == "reference":
         line = run_reference_arm(args, rank, world)

@@ -622,3 +622,18 @@ def test_grouped_argument_errors_enqueue_nothing():
         torch.cuda.synchronize()
         for c, b0 in zip(cases, before):
             assert bits_equal(c.views()[2], b0), bad
+
+
+@pytest.mark.parametrize("dtype", [F32, F64])
+@pytest.mark.parametrize("tr", TRANS)
+def test_elongated_in_domain_shapes(dtype, tr):
+    """Shapes inside the small-GEMM domain whose single problem does not fit
+    the slab family's shared memory (16 x 16 x 2000, 8 x 8 x 8000): the
+    planner streams them through the K-streamed families instead of failing."""
+    for (M, N, K) in ((16, 16, 2000), (8, 8, 8000), (80, 4, 1600)):
+        if tr == "TN" and M * N * K > 32768:
+            continue
+        c = Case(dtype, tr[0], tr[1], M, N, K, 300, 9, 1.0, 0.5)
+        c.run()
+        torch.cuda.synchronize()
+        c.check(sample_ids(c.batch, 64, 32))

@@ -115,3 +115,97 @@ def test_bench_reference_arm_under_torchrun_world2():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+
+
+def _config5_worker(rank, world, port, out):
+    """The bench's own config-5 sharding code path (bench.plan_chunks) on one
+    gloo rank: the chunks it would call, their generated inputs (global ids)
+    and the oracle's results on a sample of them, gathered to rank 0."""
+    import sys
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    import datagen
+    import oracle
+    shapes, _ = bench.workload(5)
+    # a small stand-in HBM so that every shape is also chunked inside a shard
+    chunks = bench.plan_chunks(shapes, 5, rank, world, hbm_cap=64 << 20)
+    spans = [(s.name(), lo, cnt) for s, lo, cnt in chunks]
+    # inputs + results of the first and last problem of every chunk (the
+    # shard / chunk boundaries), fp64 n = 16 shapes only (oracle cost)
+    res = []
+    for s, lo, cnt in chunks:
+        if s.M != 16:
+            continue
+        for g in (lo, lo + cnt - 1):
+            ids = np.array([g])
+            A = datagen.fill_host(s.seed, 0, np.float64, 16, 16, 16, 256, ids)
+            B = datagen.fill_host(s.seed, 1, np.float64, 16, 16, 16, 256, ids)
+            ref, _, _ = oracle.ref_gemm(s.tr[0], s.tr[1], 16, 16, 16, 1.0, A, 16, 256, B, 16, 256, 0.0, None, 16,
+                                        256, 1, nthreads=1)
+            res.append((s.name(), g, ref))
+    allspans = [None] * world
+    allres = [None] * world
+    dist.all_gather_object(allspans, spans)
+    dist.all_gather_object(allres, res)
+    if rank == 0:
+        out.put((allspans, allres))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_config5_strong_scaling_shards_under_gloo_world2():
+    """Row e (BASELINE config 5): under world size 2 the bench
+    shards the FIXED global batch of 2,000,000 into contiguous per-rank
+    ranges (dist.shard_range), chunked, disjoint and covering every problem
+    exactly once; the shard-boundary problems' inputs (generated by global
+    id) and oracle results equal the unsharded ones bitwise."""
+    import datagen
+    import oracle
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_config5_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    allspans, allres = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    per_shape = {}
+    for r, spans in enumerate(allspans):
+        lo_r, hi_r = shard_range(2_000_000, r, world)
+        for name, lo, cnt in spans:
+            assert lo_r <= lo and lo + cnt <= hi_r, (r, name, lo, cnt)
+            per_shape.setdefault(name, []).append((lo, cnt))
+    assert len(per_shape) == 12
+    for name, sp in per_shape.items():
+        sp.sort()
+        assert sp[0][0] == 0 and sum(c for _, c in sp) == 2_000_000
+        for (a, c), (b, _) in zip(sp[:-1], sp[1:]):
+            assert a + c == b, name
+    n = 0
+    for res in allres:
+        for name, g, ref in res:
+            tr = name.split("_")[1]
+            ids = np.array([g])
+            A = datagen.fill_host(4, 0, np.float64, 16, 16, 16, 256, ids)
+            B = datagen.fill_host(4, 1, np.float64, 16, 16, 16, 256, ids)
+            one, _, _ = oracle.ref_gemm(tr[0], tr[1], 16, 16, 16, 1.0, A, 16, 256, B, 16, 256, 0.0, None, 16, 256, 1,
+                                        nthreads=1)
+            assert np.array_equal(one, ref), (name, g)
+            n += 1
+    assert n >= 8
+
+
+def test_bench_rejects_gpus_world_mismatch():
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=120, cwd=root,
+                       env=dict(os.environ, WORLD_SIZE="1"))
+    assert r.returncode != 0 and "WORLD_SIZE" in (r.stderr + r.stdout)
