@@ -542,14 +542,22 @@ __device__ __forceinline__ void ks_dmma_class_loop(const IaatKsParams &p, const 
     const int pc = min(pl, P - 1);
     // per-lane offsets of fragment element k = t (step 0 of a chunk); step s
     // adds 4 k-rows (MN-major) or two 16-byte chunks (K-major, via the XOR)
+    // K-major (swizzled) operands: MMA row g reads smem row pi(g) = 2g mod 8
+    // (+1 for g >= 4) of its 8-row block.  A quarter-warp (g = 0..3 or 4..7,
+    // t = 0..3) then reads rows whose swizzle phases {0,2,4,6} / {1,3,5,7}
+    // XOR the chunk pair {2st, 2st+1} into 8 different 16-byte chunks --
+    // conflict-free, where g -> row g put two lanes on one bank (ncu round 1:
+    // 43 % of the shared wavefronts were conflicts).  The permutation is
+    // undone in the epilogue (it only relabels C rows / columns).
+    const int gA = AK ? (((2 * g) & 7) | (g >> 2)) : g, gB = BK ? (((2 * g) & 7) | (g >> 2)) : g;
     uint32_t oa[WM], ob[WN];
 #pragma unroll
     for (int mi = 0; mi < WM; ++mi)
-        oa[mi] = AK ? ks_f64_off<true>(pc * M + row0 + 8 * mi + g, t, 0, 0)
+        oa[mi] = AK ? ks_f64_off<true>(pc * M + row0 + 8 * mi + gA, t, 0, 0)
                     : ks_f64_off<false>(row0 + 8 * mi + g, t, p.a_pitch, pc * kc);
 #pragma unroll
     for (int nj = 0; nj < WN; ++nj)
-        ob[nj] = BK ? ks_f64_off<true>(pc * N + col0 + 8 * nj + g, t, 0, 0)
+        ob[nj] = BK ? ks_f64_off<true>(pc * N + col0 + 8 * nj + gB, t, 0, 0)
                     : ks_f64_off<false>(col0 + 8 * nj + g, t, p.b_pitch, pc * kc);
     const uint32_t a_step = AK ? 0u : (uint32_t)(4 * p.a_pitch * 8), b_step = BK ? 0u : (uint32_t)(4 * p.b_pitch * 8);
     const double alpha = p.alpha, beta = p.beta;
@@ -601,6 +609,13 @@ __device__ __forceinline__ void ks_dmma_class_loop(const IaatKsParams &p, const 
         }
         if (active && !(dbg & 2)) {
             double *C = reinterpret_cast<double *>(p.C + (b0 + pl) * scb);
+            // lane (g, t) holds D'[g][2t], D'[g][2t+1]: C column col0 + 8 nj +
+            // gB, C rows row0 + 8 mi + the A-side rows of MMA columns 2t,
+            // 2t+1 (pi(2t), pi(2t+1) when A is K-major: not adjacent, so
+            // scalar accesses; adjacent otherwise: one 16-byte access)
+            const int r0 = AK ? (((4 * t) & 7) | ((2 * t) >> 2)) : 2 * t;
+            const int r1 = AK ? (((4 * t + 2) & 7) | ((2 * t + 1) >> 2)) : 2 * t + 1;
+            const bool vec = c_vec && !AK;
             // per block row: all C_in loads of the row before its stores
             // (overlapped latencies, bounded registers)
 #pragma unroll
@@ -609,12 +624,12 @@ __device__ __forceinline__ void ks_dmma_class_loop(const IaatKsParams &p, const 
                 if (!beta_zero) {
 #pragma unroll
                     for (int nj = 0; nj < WN; ++nj) {
-                        const double *cp = C + (row0 + 8 * mi + 2 * t) + (int64_t)(col0 + 8 * nj + g) * ldc;
-                        if (c_vec) {
-                            ldg_vec_cs<double>(cp, ci[nj]);
+                        const double *cp = C + (row0 + 8 * mi) + (int64_t)(col0 + 8 * nj + gB) * ldc;
+                        if (vec) {
+                            ldg_vec_cs<double>(cp + r0, ci[nj]);
                         } else {
-                            ci[nj][0] = ldg_cs(cp);
-                            ci[nj][1] = ldg_cs(cp + 1);
+                            ci[nj][0] = ldg_cs(cp + r0);
+                            ci[nj][1] = ldg_cs(cp + r1);
                         }
                     }
                 }
@@ -625,12 +640,12 @@ __device__ __forceinline__ void ks_dmma_class_loop(const IaatKsParams &p, const 
                     for (int h = 0; h < 2; ++h)
                         o[h] = beta_zero ? mul_rn(alpha, acc[mi][nj][h])
                                          : fma_rn(alpha, acc[mi][nj][h], mul_rn(beta, ci[nj][h]));
-                    double *cp = C + (row0 + 8 * mi + 2 * t) + (int64_t)(col0 + 8 * nj + g) * ldc;
-                    if (c_vec) {
-                        stg_vec_cs<double>(cp, o);
+                    double *cp = C + (row0 + 8 * mi) + (int64_t)(col0 + 8 * nj + gB) * ldc;
+                    if (vec) {
+                        stg_vec_cs<double>(cp + r0, o);
                     } else {
-                        stg_cs(cp, o[0]);
-                        stg_cs(cp + 1, o[1]);
+                        stg_cs(cp + r0, o[0]);
+                        stg_cs(cp + r1, o[1]);
                     }
                 }
             }

@@ -66,7 +66,7 @@ def main():
         "square_heldout_mean_frac": float(np.mean([r["frac"] for r in sq])),
         "square_tuned_neighbours_mean_frac": float(np.mean([np.mean(r["tuned_neighbours_frac"]) for r in sq])),
         "random_mean_frac": float(np.mean([r["frac"] for r in out if r not in sq])),
-        "within_10pct_of_neighbours": sum(r["frac"] >= 0.9 * np.mean(r["tuned_neighbours_frac"]) for r in sq),
+        "within_10pct_of_neighbours": int(sum(r["frac"] >= 0.9 * np.mean(r["tuned_neighbours_frac"]) for r in sq)),
         "square_count": len(sq),
     }
     with open(a.out, "w") as f:
