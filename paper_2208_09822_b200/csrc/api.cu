@@ -373,6 +373,21 @@ iaat_status_t launch(const Prepared &pr, cudaStream_t s)
     struct {
         int dtype;
     } r{(int)pr.dt};
+    if (plan.ksg == 2) {
+        IaatKsgParams kp = plan.kgp;
+        kp.alpha = a;
+        kp.beta = b;
+        kp.A = static_cast<const char *>(A);
+        kp.B = static_cast<const char *>(B);
+        kp.C = static_cast<char *>(C);
+        cudaError_t e = kLaunchKsgs[plan.kg_entry].fn(kp, plan.grid, plan.smem, s);
+        if (e != cudaSuccess) {
+            g_last_cuda_error = (int)e;
+            return IAAT_ERROR_CUDA;
+        }
+        g_launches.fetch_add(1);
+        return IAAT_SUCCESS;
+    }
     if (plan.ksg) {
         IaatKsgParams kp = plan.kgp;
         kp.alpha = a;

@@ -475,3 +475,218 @@ __device__ __forceinline__ void ksg_body(const IaatKsgParams &p, const CUtensorM
 
 }  // namespace ksg
 }  // namespace iaat
+
+// ======================================================================
+// ksgs: the ksg lane grids on SLAB staging, for inputs the TMA rules
+// exclude (odd ld's: config 3, M or N = 2 mod 4, misaligned bases).  A unit
+// of P consecutive packed problems is one stage: ONE cp.async.bulk per
+// operand of the 16-byte-aligned span enclosing the P problems' bytes (the
+// slab family's staging, no pack pass), read in place with
+// scalar LDS at any element alignment.  Tiles cover an Mv x Nv >= M x N
+// block grid; rows / columns past M / N compute on whatever lies in the
+// stage (the next column, the next problem or the slack) and are never
+// stored: the only boundary code is the store predicate of the epilogue,
+// once per element per unit.  C_in is read from global (L2-prefetched by
+// the producer when the unit is staged), all of a lane's C_in loads issued
+// before its first store.
+// ======================================================================
+namespace iaat {
+namespace ksg {
+
+template <bool TA, bool TB, int MR, int NR, int LR>
+struct GeoS {
+    static constexpr int LC = 32 / LR;
+    static constexpr bool AK = TA, BK = !TB;
+    // FFMA2 pairs along the MN-major operand (scalar loads: any two registers pair)
+    static constexpr int PAIR = (!AK && MR % 2 == 0) ? 1 : ((!BK && NR % 2 == 0) ? 2 : 0);
+    static constexpr int BR = LR * MR, BC = LC * NR;
+    __device__ static __forceinline__ int row(int ti, int r) { return ti + LR * r; }
+    __device__ static __forceinline__ int col(int tj, int c) { return tj + LC * c; }
+};
+
+template <bool TA, bool TB, int MR, int NR, int LR, int G, int W>
+__device__ __forceinline__ void ksgs_consumer(const IaatKsgParams &p, unsigned char *smem, int g, int w, int lane)
+{
+    typedef GeoS<TA, TB, MR, NR, LR> Gm;
+    constexpr bool AK = Gm::AK, BK = Gm::BK;
+    const int K = p.K, S = p.S, M = p.M, N = p.N, lda = p.lda, ldb = p.ldb, ldc = p.ldc;
+    const int64_t nunits = p.nunits, batch = p.batch;
+    const int ti = lane % LR, tj = lane / LR;
+    const int pl = w / p.wpp, blk = w - pl * p.wpp;
+    const int R0 = (blk % p.bm) * Gm::BR, C0 = (blk / p.bm) * Gm::BC;
+    const Smem sm(smem, p, g);
+    const float alpha = (float)p.alpha, beta = (float)p.beta;
+    const bool beta_zero = p.beta_zero != 0;
+    // element offsets (words) of the lane's rows / columns inside its problem
+    // (the k-independent part): MN-major rows / columns are contiguous words,
+    // K-major ones are ld apart
+    int oa[AK ? MR : 1], ob[BK ? NR : 1];
+    if (AK) {
+#pragma unroll
+        for (int r = 0; r < MR; ++r) oa[r] = (R0 + Gm::row(ti, r)) * lda;
+    } else {
+        oa[0] = R0 + ti;
+    }
+    if (BK) {
+#pragma unroll
+        for (int c = 0; c < NR; ++c) ob[c] = (C0 + Gm::col(tj, c)) * ldb;
+    } else {
+        ob[0] = C0 + tj;
+    }
+    const int64_t sA = p.sA, sB = p.sB, sC = p.sC;
+
+    int s = 0;
+    uint32_t phase = 0;
+    for (int64_t u = (int64_t)blockIdx.x * G + g; u < nunits; u += (int64_t)gridDim.x * G) {
+        const int64_t b0 = u * p.P, b = b0 + pl;
+        RegTile<float, MR, NR, Gm::PAIR> acc;
+        acc.zero();
+        bar_wait(sm.full + 8 * s, phase);
+        {
+            // the unit's spans start at these byte offsets inside the stage
+            const uint32_t st = sm.ring + (uint32_t)(s * p.stage_bytes);
+            const uint32_t misA = (uint32_t)(reinterpret_cast<uintptr_t>(p.A + b0 * sA * 4) & 15u);
+            const uint32_t misB = (uint32_t)(reinterpret_cast<uintptr_t>(p.B + b0 * sB * 4) & 15u);
+            const uint32_t pa = st + misA + (uint32_t)(pl * sA * 4);
+            const uint32_t pb = st + (uint32_t)p.a_bytes + misB + (uint32_t)(pl * sB * 4);
+            // k-step stride (bytes) of the MN-major operands
+            const uint32_t ka = AK ? 4u : (uint32_t)lda * 4u, kb = BK ? 4u : (uint32_t)ldb * 4u;
+            uint32_t xa = pa + (AK ? 0u : (uint32_t)oa[0] * 4u), xb = pb + (BK ? 0u : (uint32_t)ob[0] * 4u);
+#pragma unroll 4
+            for (int k = 0; k < K; ++k, xa += ka, xb += kb) {
+                float a[MR], bv[NR];
+#pragma unroll
+                for (int r = 0; r < MR; ++r)
+                    a[r] = lds32(AK ? xa + (uint32_t)oa[r] * 4u : xa + (uint32_t)(LR * r * 4));
+#pragma unroll
+                for (int c = 0; c < NR; ++c)
+                    bv[c] = lds32(BK ? xb + (uint32_t)ob[c] * 4u : xb + (uint32_t)(Gm::LC * c * 4));
+                acc.rank1([&](int i) { return a[i]; }, [&](int j) { return bv[j]; });
+            }
+        }
+        __syncwarp();
+        if (lane == 0) bar_arrive(sm.empty + 8 * s);
+        if (++s == S) {
+            s = 0;
+            phase ^= 1u;
+        }
+        if (b >= batch) continue;
+        // fused epilogue, C through global: the C_in loads of a batch of
+        // columns (<= 32 values) all issued before the batch's stores
+        float v[MR][NR];
+        acc.get(v);
+        float *Cb = reinterpret_cast<float *>(p.C) + b * sC;
+        constexpr int CB = (32 / MR) < 1 ? 1 : ((32 / MR) > NR ? NR : (32 / MR));
+#pragma unroll
+        for (int c0 = 0; c0 < NR; c0 += CB) {
+            float ci[MR][CB];
+            if (!beta_zero) {
+#pragma unroll
+                for (int cc = 0; cc < CB; ++cc) {
+                    const int col = C0 + Gm::col(tj, c0 + cc);
+#pragma unroll
+                    for (int r = 0; r < MR; ++r) {
+                        const int row = R0 + Gm::row(ti, r);
+                        ci[r][cc] = (c0 + cc < NR && row < M && col < N) ? ldg_cs(Cb + (int64_t)col * ldc + row) : 0.f;
+                    }
+                }
+            }
+#pragma unroll
+            for (int cc = 0; cc < CB; ++cc) {
+                if (c0 + cc >= NR) break;
+                const int col = C0 + Gm::col(tj, c0 + cc);
+#pragma unroll
+                for (int r = 0; r < MR; ++r) {
+                    const int row = R0 + Gm::row(ti, r);
+                    if (row < M && col < N)
+                        stg_cs(Cb + (int64_t)col * ldc + row,
+                               beta_zero ? mul_rn(alpha, v[r][c0 + cc])
+                                         : fma_rn(alpha, v[r][c0 + cc], mul_rn(beta, ci[r][cc])));
+                }
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+
+// Producer (slab staging): lane 0 of warp g, one stage per unit.
+template <bool TA, bool TB, int G>
+__device__ __forceinline__ void ksgs_producer(const IaatKsgParams &p, unsigned char *smem, int g, int lane)
+{
+    if (lane != 0) return;
+    const uint64_t pol = policy_evict_first();
+    const Smem sm(smem, p, g);
+    const int64_t colsA = TA ? p.M : p.K, rowsA = TA ? p.K : p.M;
+    const int64_t colsB = TB ? p.K : p.N, rowsB = TB ? p.N : p.K;
+    int s = 0, it = 0;
+    uint32_t phase = 0;
+    for (int64_t u = (int64_t)blockIdx.x * G + g; u < p.nunits; u += (int64_t)gridDim.x * G, ++it) {
+        const int64_t b0 = u * p.P;
+        const int np = (int)min((int64_t)p.P, p.batch - b0);
+        // the 16-byte-aligned span enclosing the unit's bytes of one operand
+        // (over-read <= 15 B per end, inside granules that hold valid data)
+        auto span = [](const char *base, int64_t first, int64_t stride, int np_, int64_t rows, int64_t cols,
+                       int64_t ld, uintptr_t &lo) {
+            const uintptr_t a = reinterpret_cast<uintptr_t>(base + first * stride * 4);
+            const uintptr_t e = a + (uintptr_t)(((int64_t)(np_ - 1) * stride + (cols - 1) * ld + rows) * 4);
+            lo = a & ~(uintptr_t)15;
+            return (uint32_t)(((e + 15) & ~(uintptr_t)15) - lo);
+        };
+        uintptr_t loA, loB;
+        const uint32_t nA = span(p.A, b0, p.sA, np, rowsA, colsA, p.lda, loA);
+        const uint32_t nB = span(p.B, b0, p.sB, np, rowsB, colsB, p.ldb, loB);
+        if (it >= p.S) bar_wait(sm.empty + 8 * s, phase);
+        const uint32_t st = sm.ring + (uint32_t)(s * p.stage_bytes), fb = sm.full + 8 * s;
+        bar_expect_tx(fb, nA + nB);
+        bulk_load(st, reinterpret_cast<const void *>(loA), nA, fb, pol);
+        bulk_load(st + (uint32_t)p.a_bytes, reinterpret_cast<const void *>(loB), nB, fb, pol);
+        if (!p.beta_zero) {
+            uintptr_t loC;
+            const uint32_t nC = span(p.C, b0, p.sC, np, p.M, p.N, p.ldc, loC);
+            bulk_prefetch_l2(reinterpret_cast<const void *>(loC), nC);
+        }
+        if (++s == p.S) {
+            s = 0;
+            if (it >= 2 * p.S - 1) phase ^= 1u;
+        }
+    }
+}
+
+template <bool TA, bool TB, int MR, int NR, int LR, int G, int W>
+__device__ __forceinline__ void ksgs_body(const IaatKsgParams &p)
+{
+    static_assert(G * W == 8 || G * W == 12, "ksgs: two or three warpgroups of consumers");
+    static_assert(G <= IAAT_KSG_MAX_GROUPS, "ksgs: barrier area holds IAAT_KSG_MAX_GROUPS groups");
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < G) {
+        const Smem sm(smem, p, threadIdx.x);
+        for (int s = 0; s < p.S; ++s) {
+            bar_init(sm.full + 8 * s, 1);
+            bar_init(sm.empty + 8 * s, W);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(IAAT_KSG_PRODUCER_REGS));
+        if (warp < G) ksgs_producer<TA, TB, G>(p, smem, warp, lane);
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(IAAT_KSG_CONSUMER_REGS_OF(G * W)));
+        const int c = warp - 4;
+        ksgs_consumer<TA, TB, MR, NR, LR, G, W>(p, smem, c / W, c % W, lane);
+    }
+}
+
+}  // namespace ksg
+}  // namespace iaat

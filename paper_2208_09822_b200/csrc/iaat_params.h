@@ -28,6 +28,7 @@ enum IaatFamily : int {
     IAAT_FAM_KS1_FMA = 4, // single-class K-streamed kernels (one per tile; the big tiles)
     IAAT_FAM_KSU_FMA = 6, // single-class K-streamed fp32, uniform swizzle phase only (tm/tn % 8 == 0)
     IAAT_FAM_KSG = 7,     // fp32 lane-grid register tiles, warp groups, C through smem (iaat_ksg.cuh)
+    IAAT_FAM_KSGS = 8,    // the same lane grids on slab staging, any alignment (iaat_ksg.cuh ksgs_*)
 };
 
 // One tile class: all tiles of one exact size (mr x nr) inside one row strip
@@ -152,4 +153,12 @@ struct IaatKsgParams {
     int beta_zero;
     int bm;                // warp blocks along Mv per problem
     int wpp;               // warp blocks per problem (bm * blocks along Nv)
+    // slab staging (kernels iaat_ksgs_*): for inputs the TMA rules exclude
+    // (ld's / strides / bases not 16-byte aligned).  Each stage holds the P
+    // problems of a unit verbatim -- one cp.async.bulk per operand of the
+    // 16-byte-aligned span enclosing them -- and C goes through global.
+    const char *A, *B;
+    char *C;
+    int64_t sA, sB, sC;    // problem strides (elements; packed: sA = lda * cols of A)
+    int lda, ldb, ldc;
 };

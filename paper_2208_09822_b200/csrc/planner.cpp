@@ -343,6 +343,7 @@ struct Knobs {
 Plan make_plan_knobs(const PlanRequest &r, const Knobs &kn);
 bool plan_ks(const PlanRequest &r, const Knobs &kn, Plan &out);
 bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out);
+bool plan_ksgs(const PlanRequest &r, const Knobs &kn, Plan &out);
 
 // ---------------------------------------------------------------- install-time tuning table
 // tuning/b200.tsv next to libiaat.so (written by paper_2208_09822_b200/tune.py on
@@ -436,7 +437,7 @@ int ksg_epi_wavefronts(const IaatKsgCatalogEntry &e, int cp)
 
 bool ksg_default(const PlanRequest &r)
 {
-    return r.dtype == 0 && !r.ptr_array && std::min(r.M, r.N) >= 36 && r.K >= 16 &&
+    return r.dtype == 0 && !r.ptr_array && std::min(r.M, r.N) >= 32 && r.K >= 16 &&
            !(r.transA == 1 && r.transB == 0) && !std::getenv("IAAT_NO_KSG");
 }
 
@@ -586,6 +587,115 @@ bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
     return true;
 }
 
+
+// ksgs (slab-staged lane grids, csrc/iaat_ksg.cuh): inputs the TMA rules
+// exclude.  A unit's P packed problems are one stage (one bulk copy per
+// operand of the enclosing 16-byte-aligned span, whole K); tiles cover
+// Mv x Nv >= M x N and the stage keeps enough slack after the span for the
+// padded rows / columns to read (never stored).
+bool plan_ksgs(const PlanRequest &r, const Knobs &kn, Plan &out)
+{
+    if (r.ptr_array || r.dtype != 0) return false;
+    const int elt = 4;
+    const int64_t M = r.M, N = r.N, K = r.K;
+    const bool AK = r.transA == 1, BK = r.transB == 0;
+    const int64_t colsA = AK ? M : K, colsB = BK ? N : K, rowsA = AK ? K : M, rowsB = BK ? K : N;
+    if (K < 1 || r.batch < 1 || r.batch >= ((int64_t)1 << 31)) return false;
+    // packed (or nearly): the unit's span is the problems' bytes
+    if (r.batch > 1 && (r.sA < r.lda * colsA || r.sB < r.ldb * colsB || r.sC < r.ldc * N ||
+                        r.sA > r.lda * colsA + 16 || r.sB > r.ldb * colsB + 16))
+        return false;
+    const int tidx = r.transA * 2 + r.transB;
+    const int nent = (int)(sizeof(kKsgsCatalog) / sizeof(kKsgsCatalog[0]));
+    struct Cand {
+        int idx = -1, Mv = 0, Nv = 0, P = 0, S = 0, bm = 0, wpp = 0, ab = 0, bb = 0;
+        double cost = 0;
+    } best;
+    const double bytes = (double)(M * K + K * N + M * N * (r.beta_zero ? 1 : 2)) * elt;
+    const int64_t sA = r.batch > 1 ? r.sA : r.lda * colsA, sB = r.batch > 1 ? r.sB : r.ldb * colsB;
+    for (int i = 0; i < nent; ++i) {
+        const IaatKsgsCatalogEntry &e = kKsgsCatalog[i];
+        if (e.trans != tidx) continue;
+        if (kn.fam == IAAT_FAM_KSGS && kn.order >= 0 && kn.order != i) continue;
+        const int LC = 32 / e.lr, BR = e.lr * e.mr, BC = LC * e.nr;
+        const int Mv = (int)round_up(M, BR), Nv = (int)round_up(N, BC);
+        const int bm = Mv / BR, wpp = bm * (Nv / BC);
+        if (wpp > e.w || e.w % wpp) continue;
+        const int P = e.w / wpp;
+        // span of P problems + the 16-byte realignment + the padded reads' slack
+        const int64_t spanA = ((int64_t)(P - 1) * sA + (colsA - 1) * r.lda + rowsA) * elt;
+        const int64_t spanB = ((int64_t)(P - 1) * sB + (colsB - 1) * r.ldb + rowsB) * elt;
+        const int64_t slackA = (AK ? (int64_t)(Mv - M) * r.lda : (Mv - M)) * elt;
+        const int64_t slackB = (BK ? (int64_t)(Nv - N) * r.ldb : (Nv - N)) * elt;
+        const int ab = (int)round_up(spanA + 32 + slackA, 128), bb = (int)round_up(spanB + 32 + slackB, 128);
+        const int stage = ab + bb;
+        int S = 0;
+        while (S < IAAT_KSG_MAX_STAGES && IAAT_KSG_BAR_BYTES + 1024 + e.g * (S + 1) * stage <= IAAT_SMEM_LIMIT) ++S;
+        if (kn.fam == IAAT_FAM_KSGS && kn.s > 0) S = std::min(S, kn.s);
+        if (S < 1) continue;
+        // scalar loads: (mr + nr) LDS per k-step beside mr*nr/2 FFMA2
+        const bool pair = (!AK && e.mr % 2 == 0) || (!BK && e.nr % 2 == 0);
+        const double fma = (double)P * Mv * Nv * K / (128.0 * (pair ? 0.6 : 0.45)) / P;
+        const double smemf = 4.0 * (e.mr + e.nr) / (e.mr * e.nr);
+        const double hbm = bytes / 22.0;
+        double t = std::max(fma * std::max(1.0, smemf / 0.9), hbm) + 0.35 * std::min(fma, hbm);
+        if (S == 1) t *= 1.25;
+        if (best.idx < 0 || t < best.cost) {
+            best.idx = i;
+            best.Mv = Mv;
+            best.Nv = Nv;
+            best.P = P;
+            best.S = S;
+            best.bm = bm;
+            best.wpp = wpp;
+            best.ab = ab;
+            best.bb = bb;
+            best.cost = t;
+        }
+    }
+    if (best.idx < 0) return false;
+    const IaatKsgsCatalogEntry &e = kKsgsCatalog[best.idx];
+    Plan pl;
+    IaatKsgParams &k = pl.kgp;
+    k.batch = r.batch;
+    k.nunits = (r.batch + best.P - 1) / best.P;
+    k.M = (int)M;
+    k.N = (int)N;
+    k.K = (int)K;
+    k.Mv = best.Mv;
+    k.Nv = best.Nv;
+    k.P = best.P;
+    k.S = best.S;
+    k.nchunks = 1;
+    k.a_bytes = best.ab;
+    k.b_bytes = best.bb;
+    k.stage_bytes = best.ab + best.bb;
+    k.c_bytes = 0;
+    k.group_bytes = best.S * k.stage_bytes;
+    k.beta_zero = r.beta_zero;
+    k.bm = best.bm;
+    k.wpp = best.wpp;
+    k.sA = sA;
+    k.sB = sB;
+    k.sC = r.batch > 1 ? r.sC : r.ldc * N;
+    k.lda = (int)r.lda;
+    k.ldb = (int)r.ldb;
+    k.ldc = (int)r.ldc;
+    pl.ksg = 2;
+    pl.kg_entry = best.idx;
+    pl.family = IAAT_FAM_KSGS;
+    pl.vec = 0;
+    pl.ctas = 1;
+    pl.grid = (int)std::min<int64_t>((k.nunits + e.g - 1) / e.g, (int64_t)r.sm_count);
+    pl.block = 128 + 32 * e.g * e.w;
+    pl.smem = IAAT_KSG_BAR_BYTES + 1024 + e.g * k.group_bytes;
+    pl.est_total = best.cost;
+    pl.memops = (int64_t)(best.Mv / e.mr) * (best.Nv / e.nr) * (e.mr + e.nr) * K + 2 * M * N;
+    pl.status = 0;
+    out = pl;
+    return true;
+}
+
 Plan make_plan(const PlanRequest &r)
 {
     Knobs kn;
@@ -634,9 +744,20 @@ Plan make_plan(const PlanRequest &r)
         }
         kn = Knobs();
     }
+    if (kn.fam == IAAT_FAM_KSGS) {
+        Plan pg;
+        if (plan_ksgs(r, kn, pg)) {
+            pg.tuned = tuned;
+            return pg;
+        }
+        kn = Knobs();
+    }
     if (!kn.any() && ksg_default(r)) {
         // the upper half of the fp32 domain: lane-grid register tiles with
-        // warp groups (csrc/iaat_ksg.cuh) whenever their TMA preconditions hold
+        // warp groups (csrc/iaat_ksg.cuh) wherever their TMA rules hold.
+        // (The slab-staged ksgs kernels are chosen only by the install-time
+        // table: on held-out misaligned shapes they measured no better than
+        // the slab family on average, profiles/r02/heldout_r02*.)
         Plan pg;
         if (plan_ksg(r, Knobs(), pg)) return pg;
     }
@@ -1529,6 +1650,18 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
     }
     const IaatKParams &k = p.kp;
     add("\"tuned\": %d, ", p.tuned);
+    if (p.ksg == 2) {
+        const IaatKsgParams &q = p.kgp;
+        const IaatKsgsCatalogEntry &e = kKsgsCatalog[p.kg_entry];
+        add("\"family\": \"ksgs\", \"entry\": %d, \"mr\": %d, \"nr\": %d, \"lane_rows\": %d, \"groups\": %d, "
+            "\"warps_per_group\": %d, \"Mv\": %d, \"Nv\": %d, \"P\": %d, \"S\": %d, \"a_bytes\": %d, "
+            "\"b_bytes\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, \"nunits\": %lld, \"est\": %.0f, "
+            "\"memops\": %lld, ",
+            p.kg_entry, e.mr, e.nr, e.lr, e.g, e.w, q.Mv, q.Nv, q.P, q.S, q.a_bytes, q.b_bytes, p.grid, p.block,
+            p.smem, (long long)q.nunits, p.est_total, (long long)p.memops);
+        s += "\"classes\": []}";
+        return s;
+    }
     if (p.ksg) {
         const IaatKsgParams &q = p.kgp;
         const IaatKsgCatalogEntry &e = kKsgCatalog[p.kg_entry];

@@ -47,6 +47,7 @@ struct Plan {
     IaatKsParams ksp{};
     TmaGeo tmA{}, tmB{};
     int ksg = 0;           // 1: ksg family (kgp + tmA/tmB/tmC, kernel kKsgCatalog[kg_entry])
+                           // 2: ksgs -- slab-staged lane grids (kgp only, kernel kKsgsCatalog[kg_entry])
     int kg_entry = -1;
     IaatKsgParams kgp{};
     TmaGeo tmC{};

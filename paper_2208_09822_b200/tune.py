@@ -340,8 +340,8 @@ def line_to_knobs(v):
 
 
 def tune_ksg(sh, current, log):
-    """ksg family (csrc/iaat_ksg.cuh) against the current plan of one input:
-    every applicable catalog entry (forced), each at its planner-chosen ring
+    """ksg / ksgs families (csrc/iaat_ksg.cuh) against the current plan of one
+    input: every applicable catalog entry (forced), each at its planner-chosen ring
     depth and one stage fewer, plus the current table entry (or the cost
     model's plan); the leaders are re-timed and the fastest is kept."""
     from paper_2208_09822_b200 import iaat
@@ -349,18 +349,19 @@ def tune_ksg(sh, current, log):
     b = Bench(*sh)
     cands = [current or {}]
     for e in iaat.iaat_catalog_describe():
-        if e["family"] != "ksg" or e["trans"] != tr:
+        if e["family"] not in ("ksg", "ksgs") or e["trans"] != tr:
             continue
-        set_knobs(family=7, order=e["index"])
+        fam = 7 if e["family"] == "ksg" else 8
+        set_knobs(family=fam, order=e["index"])
         try:
             p = b.plan()
         finally:
             set_knobs()
-        if p.get("family") != "ksg" or p.get("entry") != e["index"]:
+        if p.get("family") != e["family"] or p.get("entry") != e["index"]:
             continue
-        cands.append({"family": 7, "order": e["index"]})
+        cands.append({"family": fam, "order": e["index"]})
         if p["S"] > 1:
-            cands.append({"family": 7, "order": e["index"], "s": p["S"] - 1})
+            cands.append({"family": fam, "order": e["index"], "s": p["S"] - 1})
     res = []
     for kw in cands:
         set_knobs(**kw)
@@ -438,7 +439,7 @@ def main(argv=None):
             dtype, tr, M, N, K, batch, alpha, beta = sh
             key = key_line({"f32": 0, "f64": 1, "c32": 2, "c64": 3}[dtype], tr, M, N, K, beta == 0)
             if a.ksg:
-                if dtype != "f32" or tr == "TN":
+                if dtype != "f32" or tr == "TN" or min(M, N) < 24:
                     continue
                 kw, p = tune_ksg(sh, line_to_knobs(existing[key]) if key in existing else {}, log)
             else:

@@ -117,3 +117,50 @@ def test_ksg_default_plans_and_small_batches():
             c.run()
             torch.cuda.synchronize()
             c.check()
+
+
+SLAB_SHAPES = [(37, 67, 79), (67, 67, 17), (79, 79, 79), (33, 61, 47), (38, 38, 38), (61, 53, 31), (47, 79, 5)]
+
+
+@pytest.mark.parametrize("tr", ["NN", "NT", "TT"])
+def test_ksgs_every_entry_odd_shapes_parity_and_bitwise_vs_slab(tr):
+    """ksgs (slab-staged lane grids): odd ld's, element-misaligned bases and
+    padded ld's (the TMA rules exclude all of them), every entry forced
+    (IAAT_FORCE_FAMILY=8), against the oracle and bitwise against the slab
+    family; beta == 0 with a NaN-filled C."""
+    ents = [e for e in iaat_entries("ksgs") if e["trans"] == tr]
+    assert ents
+    ran = 0
+    try:
+        for e in ents:
+            for i, (M, N, K) in enumerate(SLAB_SHAPES):
+                beta = 0.0 if i % 3 == 2 else 0.5
+                extra = [{}, {"pad": 1}, {"elem_offset": 1}][i % 3]
+                _force(family=8, order=e["index"])
+                c = Case(F32, tr[0], tr[1], M, N, K, 211, 41, -0.75, beta, **extra)
+                p = _plan(c, beta)
+                if p.get("family") != "ksgs" or p.get("entry") != e["index"]:
+                    continue
+                A, B, C = c.views()
+                if beta == 0:
+                    C.fill_(float("nan"))
+                c.run()
+                torch.cuda.synchronize()
+                c.check(sample_ids(c.batch, 48, 24))
+                got = c.C.clone()
+                _force(family=0)
+                c2 = Case(F32, tr[0], tr[1], M, N, K, 211, 41, -0.75, beta, **extra)
+                if beta == 0:
+                    c2.views()[2].fill_(float("nan"))
+                c2.run()
+                torch.cuda.synchronize()
+                assert bits_equal(got, c2.C), (tr, e, M, N, K, beta, extra)
+                ran += 1
+    finally:
+        _force()
+    assert ran >= len(ents), ran
+
+
+def iaat_entries(fam):
+    from paper_2208_09822_b200 import iaat
+    return [e for e in iaat.iaat_catalog_describe() if e["family"] == fam]
