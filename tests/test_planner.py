@@ -39,6 +39,18 @@ def plan(dt, tr, M, N, K, batch=10000, beta0=False, align=256, pad=0):
 KSG = {e["index"]: e for e in CAT if e["family"] == "ksg"}
 
 
+KSGS = {e["index"]: e for e in CAT if e["family"] == "ksgs"}
+
+
+def check_ksgs_plan(p, tr, M, N):
+    e = KSGS[p["entry"]]
+    br, bc = e["lr"] * e["mr"], (32 // e["lr"]) * e["nr"]
+    assert e["trans"] == tr and p["Mv"] % br == 0 and p["Nv"] % bc == 0
+    assert M <= p["Mv"] < M + br and N <= p["Nv"] < N + bc
+    assert (p["Mv"] // br) * (p["Nv"] // bc) * p["P"] == e["w"]
+    assert p["smem"] <= 227 * 1024 and p["S"] >= 1
+
+
 def check_ksg_plan(p, tr, M, N):
     """ksg (csrc/iaat_ksg.cuh): one lane-grid class whose warp blocks tile the
     Mv x Nv problem exactly; Mv - M, Nv - N < one warp block (the copy
@@ -62,6 +74,9 @@ def check_plan(p, dt, tr, M, N):
     assert p["status"] == 0, p
     if p.get("family") == "ksg":
         check_ksg_plan(p, tr, M, N)
+        return
+    if p.get("family") == "ksgs":
+        check_ksgs_plan(p, tr, M, N)
         return
     cover = np.zeros((M, N), dtype=np.int32)
     dname = "f32" if dt == 0 else "f64"
@@ -197,6 +212,9 @@ def test_catalog_register_budget():
             assert e["mr"] * e["nr"] <= 128 and 32 % e["lr"] == 0
             assert e["g"] * e["w"] in (8, 12) and e["g"] <= 4 and e["kc"] in (16, 32) and e["ku"] in (2, 4)
             assert tuple(e[k] for k in ("trans", "mr", "nr", "lr", "kc", "ku", "g", "w")) == gen.KSG_TILES[e["index"]]
+        elif e["family"] == "ksgs":
+            assert e["dtype"] == "f32" and e["trans"] != "TN" and e["mr"] * e["nr"] <= 100
+            assert tuple(e[k] for k in ("trans", "mr", "nr", "lr", "g", "w")) == gen.KSGS_TILES[e["index"]]
         elif e["family"] == "ks_dmma" and e["dtype"] == "c64":
             assert (e["mr"] // 8, e["nr"] // 8) in gen.KSZ_TILES
         elif e["family"] in ("ks_fma", "ks1_fma"):
