@@ -329,7 +329,29 @@ __device__ __forceinline__ void ksg_consumer(const IaatKsgParams &p, unsigned ch
         }
         bar_wait(sm.cfull, cphase);
         cphase ^= 1u;
-        {
+        if constexpr (Gm::PAIR == 1 && !AK && Gm::VA == 2) {
+            // accumulator pairs are two adjacent C rows: one LDS.64 of C_in,
+            // FMUL2 + FFMA2 (the same two IEEE roundings per element), one STS.64
+            const unsigned long long a2 = pack_f32x2(alpha, alpha), b2 = pack_f32x2(beta, beta);
+#pragma unroll
+            for (int c = 0; c < NR; ++c) {
+                const uint32_t colb = cb0 + (uint32_t)(Gm::col(tj, c) * cp * 4);
+#pragma unroll
+                for (int q = 0; q < MR / 2; ++q) {
+                    const uint32_t a = colb + (uint32_t)(Gm::row(ti, 2 * q) * 4);
+                    unsigned long long o;
+                    if (beta_zero) {
+                        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(o) : "l"(a2), "l"(acc.v[q][c]));
+                    } else {
+                        unsigned long long ci, t;
+                        asm volatile("ld.shared.b64 %0, [%1];" : "=l"(ci) : "r"(a));
+                        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(b2), "l"(ci));
+                        asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(o) : "l"(a2), "l"(acc.v[q][c]), "l"(t));
+                    }
+                    asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(o) : "memory");
+                }
+            }
+        } else {
             float v[MR][NR];
             acc.get(v);
 #pragma unroll

@@ -1,0 +1,3 @@
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -lcuda -Ipaper_2208_09822_b200/csrc -o ksg_probe_bin tools/experiments/ksg_probe.cu || exit 1
+echo "== padded C pitch"; timeout 300 ./ksg_probe_bin 2>&1
+echo "== C pitch = Mv"; PROBE_CP_NOPAD=1 timeout 300 ./ksg_probe_bin 2>&1
