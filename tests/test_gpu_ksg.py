@@ -119,10 +119,11 @@ def test_ksg_default_plans_and_small_batches():
             c.check()
 
 
+TN_SHAPES = [(31, 31, 31), (17, 17, 17), (23, 29, 19), (32, 32, 2), (13, 9, 21), (27, 27, 27), (5, 31, 29)]
 SLAB_SHAPES = [(37, 67, 79), (67, 67, 17), (79, 79, 79), (33, 61, 47), (38, 38, 38), (61, 53, 31), (47, 79, 5)]
 
 
-@pytest.mark.parametrize("tr", ["NN", "NT", "TT"])
+@pytest.mark.parametrize("tr", ["NN", "NT", "TT", "TN"])
 def test_ksgs_every_entry_odd_shapes_parity_and_bitwise_vs_slab(tr):
     """ksgs (slab-staged lane grids): odd ld's, element-misaligned bases and
     padded ld's (the TMA rules exclude all of them), every entry forced
@@ -133,7 +134,7 @@ def test_ksgs_every_entry_odd_shapes_parity_and_bitwise_vs_slab(tr):
     ran = 0
     try:
         for e in ents:
-            for i, (M, N, K) in enumerate(SLAB_SHAPES):
+            for i, (M, N, K) in enumerate(SLAB_SHAPES if tr != "TN" else TN_SHAPES):
                 beta = 0.0 if i % 3 == 2 else 0.5
                 extra = [{}, {"pad": 1}, {"elem_offset": 1}][i % 3]
                 _force(family=8, order=e["index"])
