@@ -172,12 +172,27 @@ struct Opnd {
     }
 };
 
+#ifndef IAAT_KSG_FMA_ORDER
+#define IAAT_KSG_FMA_ORDER 1
+#endif
 template <int KU, int MR, int NR, int PAIR>
 __device__ __forceinline__ void kblock_fma(RegTile<float, MR, NR, PAIR> &acc, const float (&a)[KU][MR],
                                            const float (&b)[KU][NR])
 {
+    if constexpr (PAIR == 1 && IAAT_KSG_FMA_ORDER == 1) {
+        // pair-outer order: consecutive FFMA2s share the a-pair operand
 #pragma unroll
-    for (int kk = 0; kk < KU; ++kk) acc.rank1([&](int i) { return a[kk][i]; }, [&](int j) { return b[kk][j]; });
+        for (int kk = 0; kk < KU; ++kk)
+#pragma unroll
+            for (int i = 0; i < MR / 2; ++i) {
+                const unsigned long long ap = pack_f32x2(a[kk][2 * i], a[kk][2 * i + 1]);
+#pragma unroll
+                for (int j = 0; j < NR; ++j) ffma2(acc.v[i][j], ap, pack_f32x2(b[kk][j], b[kk][j]));
+            }
+    } else {
+#pragma unroll
+        for (int kk = 0; kk < KU; ++kk) acc.rank1([&](int i) { return a[kk][i]; }, [&](int j) { return b[kk][j]; });
+    }
 }
 
 // Shared-memory map: [barriers (1 KB)] then, per group g, at the first
