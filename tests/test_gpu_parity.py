@@ -637,3 +637,28 @@ def test_elongated_in_domain_shapes(dtype, tr):
         c.run()
         torch.cuda.synchronize()
         c.check(sample_ids(c.batch, 64, 32))
+
+
+@pytest.mark.parametrize("tr", ["NN", "NT"])
+@pytest.mark.parametrize("n", [16, 64, 80])
+def test_config5_shards_bitwise_equal_unsharded(n, tr):
+    """Row e: config 5's strong-scaling shards -- each "rank" r
+    of G generates its own inputs by GLOBAL problem id over
+    dist.shard_range(B, r, G) and calls the library on them -- give C
+    bitwise equal to one unsharded call, for G = 2, 4, 8 (shard boundaries
+    included: every problem is compared)."""
+    from paper_2208_09822_b200.dist import shard_range
+    B = 20011
+    full = Case(F64, tr[0], tr[1], n, n, n, B, 4, 1.0, 0.0)
+    full.run()
+    ref = full.views()[2].clone()
+    del full
+    for G in (2, 4, 8):
+        parts = []
+        for r in range(G):
+            lo, hi = shard_range(B, r, G)
+            c = Case(F64, tr[0], tr[1], n, n, n, hi - lo, 4, 1.0, 0.0, first_id=lo)
+            c.run()
+            parts.append(c.views()[2][:(hi - lo) * c.sC].clone())
+        torch.cuda.synchronize()
+        assert bits_equal(torch.cat(parts), ref[:B * n * n]), G
