@@ -129,14 +129,30 @@ __device__ __forceinline__ uint32_t kmaj_base(int ra)
 // Fragment of one operand for one k-block of KU (2 or 4) k-steps: f[kk][r].
 // K-major: one LDS.64 / LDS.128 per element row (KU consecutive k values);
 // MN-major: one V-wide load per vector group per k-step.
-template <bool KMAJ, int R, int V, int L>
+// K-major rows of a lane are L apart; when L is a multiple of 8 every row
+// of the lane has the same swizzle phase (the 128-byte swizzle repeats every
+// 8 rows, the 64-byte one every 8 rows of 64 bytes), so one XOR on the first
+// row's base serves all rows and the rest are immediates (UNI): no per-row
+// LOP3 / IADD in the k loop (measured: the general path made NN / TT loops
+// ~9 % slower than NT's, which has no K-major operand).
+template <bool KMAJ, int R, int V, int L, int KC>
 struct Opnd {
+    static constexpr bool UNI = KMAJ && (L % 8 == 0);
     uint32_t base[KMAJ ? R : 1];  // K-major: per-row swizzled base; MN-major: first element
     uint32_t pitch;               // MN-major: bytes per k-step
     template <int KU>
     __device__ __forceinline__ void load(float (&f)[KU][R], uint32_t stage, int kb) const
     {
-        if (KMAJ) {
+        if (UNI) {
+            const uint32_t q = (uint32_t)(kb >> 2) << 4, w = (uint32_t)(kb & 3) * 4u;
+            const uint32_t x = stage + (base[0] ^ q) + (KU == 4 ? 0u : w);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t a = x + (uint32_t)(r * L * KC * 4);
+                if (KU == 4) lds128(a, f[0][r], f[KU > 1 ? 1 : 0][r], f[KU > 2 ? 2 : 0][r], f[KU > 3 ? 3 : 0][r]);
+                else lds64(a, f[0][r], f[KU > 1 ? 1 : 0][r]);
+            }
+        } else if (KMAJ) {
             const uint32_t q = (uint32_t)(kb >> 2) << 4, w = (uint32_t)(kb & 3) * 4u;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -256,8 +272,8 @@ __device__ __forceinline__ void ksg_consumer(const IaatKsgParams &p, unsigned ch
     const int R0 = (blk % p.bm) * Gm::BR, C0 = (blk / p.bm) * Gm::BC;
     const Smem sm(smem, p, g);
 
-    Opnd<AK, MR, Gm::VA, LR> oa;
-    Opnd<BK, NR, Gm::VB, Gm::LC> ob;
+    Opnd<AK, MR, Gm::VA, LR, KC> oa;
+    Opnd<BK, NR, Gm::VB, Gm::LC, KC> ob;
     if (AK) {
 #pragma unroll
         for (int r = 0; r < MR; ++r) oa.base[r] = kmaj_base<KC>(pl * Mv + R0 + Gm::row(ti, r));

@@ -438,12 +438,35 @@ def test_invalid_arguments_enqueue_nothing():
 
 
 def test_launch_uses_sm100_kernels_only():
-    """The call enqueues exactly one launch (the persistent plan)."""
+    """The call enqueues exactly one launch (the persistent plan), and the
+    kernels the device actually ran (CUDA activity trace) are this library's
+    own iaat_* kernels -- no library or fallback kernel -- for every family
+    (slab, K-streamed, ksg, fp64 DMMA); the shipped .so holds sm_100a SASS
+    only (tests/test_build.py)."""
+    import os
+    from torch.profiler import ProfilerActivity, profile
     from paper_2208_09822_b200 import iaat
     c = Case(F32, "N", "N", 32, 32, 32, 1000, 1, 1.0, 0.0)
     n0 = iaat.iaat_launch_count()
     c.run()
     assert iaat.iaat_launch_count() == n0 + 1
+    torch.cuda.synchronize()
+    cases = [Case(F32, "N", "N", 16, 16, 16, 500, 1, 1.0, 0.0), Case(F32, "N", "T", 64, 64, 64, 300, 2, 1.5, 0.5),
+             Case(F64, "N", "N", 32, 32, 32, 300, 3, 1.0, 0.0), Case(F32, "T", "T", 40, 36, 44, 129, 4, 1.5, 0.5)]
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for i, cc in enumerate(cases):
+            if i == 3:
+                os.environ["IAAT_FORCE_FAMILY"] = "2"
+            try:
+                cc.run()
+            finally:
+                os.environ.pop("IAAT_FORCE_FAMILY", None)
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+    kern = [n for n in names if "memcpy" not in n.lower() and "memset" not in n.lower()]
+    assert len([n for n in kern if "iaat" in n]) == len(cases), kern
+    assert all("iaat" in n for n in kern), kern
+    assert any("iaat_ksg_" in n for n in kern) and any("iaat_ks_" in n or "iaat_ks1_" in n for n in kern), kern
 
 
 # ---------------------------------------------------------------- K-streamed (TMA) family
