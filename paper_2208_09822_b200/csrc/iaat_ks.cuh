@@ -172,6 +172,12 @@ __device__ void ks_producer(const IaatKsParams &p, const CUtensorMap *tmA, const
     prefetch_tmap(tmA);
     prefetch_tmap(tmB);
     const uint64_t pol = policy_evict_first();
+    // K-major boxes (one kc-wide piece of each column) share a 32-byte
+    // sector with the column's next chunk: normal L2 priority keeps it
+    // (iaat_ksg.cuh ksg_producer, measured there)
+    uint64_t pol_norm;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_norm));
+    const uint64_t polA = TA ? pol_norm : pol, polB = TB ? pol : pol_norm;
     const uint32_t tx = (uint32_t)(p.a_tx + p.b_tx);
     unsigned char *ring = ks_ring(smem);
     int s = 0, it = 0;
@@ -197,10 +203,10 @@ __device__ void ks_producer(const IaatKsParams &p, const CUtensorMap *tmA, const
             mbar_arrive_expect_tx(&full[s], tx);
             const int k0 = c * p.kc;
             const int kr = p.cplx ? 2 * k0 : k0;  // complex: K-major boxes index the real (re, im) view
-            if (TA) tma_load_3d(st, tmA, kr, 0, b0, &full[s], pol);                 // A: K x M, K-major
-            else    tma_load_3d(st, tmA, 0, k0, b0, &full[s], pol);                 // A: M x K, MN-major
-            if (TB) tma_load_3d(st + p.a_bytes, tmB, 0, k0, b0, &full[s], pol);     // B: N x K, MN-major
-            else    tma_load_3d(st + p.a_bytes, tmB, kr, 0, b0, &full[s], pol);     // B: K x N, K-major
+            if (TA) tma_load_3d(st, tmA, kr, 0, b0, &full[s], polA);                 // A: K x M, K-major
+            else    tma_load_3d(st, tmA, 0, k0, b0, &full[s], polA);                 // A: M x K, MN-major
+            if (TB) tma_load_3d(st + p.a_bytes, tmB, 0, k0, b0, &full[s], polB);     // B: N x K, MN-major
+            else    tma_load_3d(st + p.a_bytes, tmB, kr, 0, b0, &full[s], polB);     // B: K x N, K-major
             if (++s == p.S) {
                 s = 0;
                 if (it >= 2 * p.S - 1) phase ^= 1u;  // lap L >= 1 waits for parity (L - 1) & 1

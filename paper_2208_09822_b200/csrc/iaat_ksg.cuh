@@ -188,6 +188,9 @@ struct Opnd {
     }
 };
 
+#ifndef IAAT_KSG_EVICT_FIRST
+#define IAAT_KSG_EVICT_FIRST 0
+#endif
 #ifndef IAAT_KSG_FMA_ORDER
 #define IAAT_KSG_FMA_ORDER 1
 #endif
@@ -432,7 +435,19 @@ __device__ __forceinline__ void ksg_producer(const IaatKsgParams &p, const CUten
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmB)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmC)) : "memory");
+    // L2 policies.  evict_first is right for data read once -- but a K-major
+    // box row (kc * 4 = 64 or 128 bytes of one column) starts at the
+    // column's own alignment, so consecutive K-chunks of a column share a
+    // 32-byte sector at their boundary; with evict_first that sector is gone
+    // before the next chunk's load and is read twice (ncu: DRAM reads +9-17 %
+    // over the operand bytes at n = 56-76).  K-major operands therefore load
+    // with normal priority (measured +5 % at n = 56 NN / TT); MN-major boxes
+    // (whole contiguous rows) and C keep evict_first.
     const uint64_t pol = policy_evict_first();
+    uint64_t pol_norm;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_norm));
+    const uint64_t polA = (TA && !IAAT_KSG_EVICT_FIRST) ? pol_norm : pol;
+    const uint64_t polB = (!TB && !IAAT_KSG_EVICT_FIRST) ? pol_norm : pol;
     const uint32_t tx = (uint32_t)(p.a_tx + p.b_tx);
     const Smem sm(smem, p, g);
     int s = 0, it = 0;
@@ -443,10 +458,10 @@ __device__ __forceinline__ void ksg_producer(const IaatKsgParams &p, const CUten
         const uint32_t st = sm.ring + (uint32_t)(s * p.stage_bytes), fb = sm.full + 8 * s;
         bar_expect_tx(fb, tx);
         const int k0 = c * KC;
-        if (TA) tma_load_3d(st, tmA, k0, 0, b0, fb, pol);
-        else tma_load_3d(st, tmA, 0, k0, b0, fb, pol);
-        if (TB) tma_load_3d(st + p.a_bytes, tmB, 0, k0, b0, fb, pol);
-        else tma_load_3d(st + p.a_bytes, tmB, k0, 0, b0, fb, pol);
+        if (TA) tma_load_3d(st, tmA, k0, 0, b0, fb, polA);
+        else tma_load_3d(st, tmA, 0, k0, b0, fb, polA);
+        if (TB) tma_load_3d(st + p.a_bytes, tmB, 0, k0, b0, fb, polB);
+        else tma_load_3d(st + p.a_bytes, tmB, k0, 0, b0, fb, polB);
         if (++s == p.S) {
             s = 0;
             if (it >= 2 * p.S - 1) phase ^= 1u;
