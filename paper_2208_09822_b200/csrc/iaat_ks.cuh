@@ -588,7 +588,9 @@ __device__ __forceinline__ void ks_dmma_class_loop(const IaatKsParams &p, const 
                 const unsigned char *sb = sa + a_bytes;
                 const int kv = min(kc, K - ch * kc);
                 const int nsteps = (kv + 3) >> 2;
-#pragma unroll 4
+                // 5x5 tiles: 100 accumulator registers leave room for two
+                // steps of fragments in flight, not four (spill-free at 168)
+#pragma unroll(WM * WN >= 25 ? 2 : 4)
                 for (int st = 0; st < nsteps; ++st) {
                     double af[WM], bf[WN];
                     // K-major: k = 4*st + t lives in 16-byte chunk 2*st + t/2 -> XOR (st << 5) on the chunk bits
