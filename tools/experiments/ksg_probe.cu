@@ -257,6 +257,14 @@ int main(int argc, char **argv)
         V("TT56_7x14_l8_k16u2_g4w2_p2_s2", true, true, 56, 56, 7, 14, 8, 16, 2, 4, 2, 2, 2),
         V("NT56_14x7_l4_k16u2_g4w2_p2_s2", false, true, 56, 56, 14, 7, 4, 16, 2, 4, 2, 2, 2),
         V("NN68_6x9_l4_k16u2_g4w3_p1_s2", false, false, 68, 72, 6, 9, 4, 16, 2, 4, 3, 1, 2),
+        // where the time goes (DBG: 1 = no staging, 2 = no epilogue, 3 = neither)
+        VD("NN80_10x10_l4_k16u2_g4w2_p1_s2_d1", false, false, 80, 80, 10, 10, 4, 16, 2, 4, 2, 1, 2, 1),
+        VD("NN80_10x10_l4_k16u2_g4w2_p1_s2_d2", false, false, 80, 80, 10, 10, 4, 16, 2, 4, 2, 1, 2, 2),
+        VD("NN80_10x10_l4_k16u2_g4w2_p1_s2_d3", false, false, 80, 80, 10, 10, 4, 16, 2, 4, 2, 1, 2, 3),
+        V("NN80_10x5_l4_k16u4_g3w4_p1_s3", false, false, 80, 80, 10, 5, 4, 16, 4, 3, 4, 1, 3),
+        VD("NN80_10x5_l4_k16u4_g3w4_p1_s3_d1", false, false, 80, 80, 10, 5, 4, 16, 4, 3, 4, 1, 3, 1),
+        VD("NN80_10x5_l4_k16u4_g3w4_p1_s3_d2", false, false, 80, 80, 10, 5, 4, 16, 4, 3, 4, 1, 3, 2),
+        VD("NN80_10x5_l4_k16u4_g3w4_p1_s3_d3", false, false, 80, 80, 10, 5, 4, 16, 4, 3, 4, 1, 3, 3),
     };
     size_t maxe = 0;
     for (auto &v : vs) {
