@@ -126,8 +126,8 @@ __device__ __forceinline__ uint32_t kmaj_base(int ra)
     return ((uint32_t)ra << 6) | ((uint32_t)((ra >> 1) & 3) << 4);
 }
 
-// Fragment of one operand for one k-block of KU (2 or 4) k-steps: f[kk][r].
-// K-major: one LDS.64 / LDS.128 per element row (KU consecutive k values);
+// Fragment of one operand for one k-block of KU (1, 2 or 4) k-steps: f[kk][r].
+// K-major: one LDS.32 / LDS.64 / LDS.128 per element row (KU consecutive k values);
 // MN-major: one V-wide load per vector group per k-step.
 // K-major rows of a lane are L apart; when L is a multiple of 8 every row
 // of the lane has the same swizzle phase (the 128-byte swizzle repeats every
@@ -150,14 +150,16 @@ struct Opnd {
             for (int r = 0; r < R; ++r) {
                 const uint32_t a = x + (uint32_t)(r * L * KC * 4);
                 if (KU == 4) lds128(a, f[0][r], f[KU > 1 ? 1 : 0][r], f[KU > 2 ? 2 : 0][r], f[KU > 3 ? 3 : 0][r]);
-                else lds64(a, f[0][r], f[KU > 1 ? 1 : 0][r]);
+                else if (KU == 2) lds64(a, f[0][r], f[KU > 1 ? 1 : 0][r]);
+                else f[0][r] = lds32(a);
             }
         } else if (KMAJ) {
             const uint32_t q = (uint32_t)(kb >> 2) << 4, w = (uint32_t)(kb & 3) * 4u;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 if (KU == 4) lds128(stage + (base[r] ^ q), f[0][r], f[KU > 1 ? 1 : 0][r], f[KU > 2 ? 2 : 0][r], f[KU > 3 ? 3 : 0][r]);
-                else lds64(stage + (base[r] ^ q) + w, f[0][r], f[KU > 1 ? 1 : 0][r]);
+                else if (KU == 2) lds64(stage + (base[r] ^ q) + w, f[0][r], f[KU > 1 ? 1 : 0][r]);
+                else f[0][r] = lds32(stage + (base[r] ^ q) + w);
             }
         } else {
 #pragma unroll

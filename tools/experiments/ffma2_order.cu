@@ -107,6 +107,82 @@ __global__ void __launch_bounds__(384, 1) kord(float *out, int K)
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// ksg NN fragment shape: k-blocks of 2, A pairs (LDS.64 per pair per k),
+// B K-major (one LDS.64 = the column's values at k and k+1), FFMA2 order
+// kk -> i -> j (kblock_fma); DB = register double buffering of k-blocks
+template <bool DB, bool RND>
+__global__ void __launch_bounds__(384, 1) kks(float *out, int K)
+{
+    extern __shared__ __align__(16) unsigned char sm[];
+    const unsigned base = (unsigned)__cvta_generic_to_shared(sm);
+    for (int i = threadIdx.x; i < 16384; i += blockDim.x) {
+        unsigned h = (unsigned)i * 2654435761u + blockIdx.x * 40503u;
+        h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+        reinterpret_cast<float *>(sm)[i] = RND ? (float)(h >> 8) * (1.0f / 8388608.0f) - 1.0f : (float)(i % 7) * 0.125f;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const unsigned sa = base + (lane & 3) * 8, sb = base + 32768 + (lane >> 2) * 64;
+    unsigned long long acc[MP][NR];
+#pragma unroll
+    for (int i = 0; i < MP; ++i)
+#pragma unroll
+        for (int j = 0; j < NR; ++j) acc[i][j] = 0ull;
+    for (int kc = 0; kc < K; kc += 16) {
+        unsigned long long a[2][2][MP];
+        float b[2][2][NR];
+        auto ld = [&](int buf, int kb) {
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+                for (int i = 0; i < MP; ++i) lds64(sa + (kb + kk) * 320 + i * 32, a[buf][kk][i]);
+#pragma unroll
+            for (int j = 0; j < NR; ++j) lds64f(sb + j * 512 + ((kb * 4) ^ ((j & 3) << 4)), b[buf][0][j], b[buf][1][j]);
+        };
+        ld(0, 0);
+#pragma unroll
+        for (int kb = 0; kb < 16; kb += 2) {
+            const int cur = DB ? (kb / 2) & 1 : 0;
+            if (DB && kb + 2 < 16) ld(cur ^ 1, kb + 2);
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+                for (int i = 0; i < MP; ++i)
+#pragma unroll
+                    for (int j = 0; j < NR; ++j) f2(acc[i][j], a[cur][kk][i], b[cur][kk][j]);
+            if (!DB && kb + 2 < 16) ld(0, kb + 2);
+        }
+    }
+    float s = 0;
+#pragma unroll
+    for (int i = 0; i < MP; ++i)
+#pragma unroll
+        for (int j = 0; j < NR; ++j) s += __uint_as_float((unsigned)acc[i][j]) + __uint_as_float((unsigned)(acc[i][j] >> 32));
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+template <bool DB, bool RND>
+void run_ks(int wps, float *o)
+{
+    auto fn = kks<DB, RND>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    const int blocks = 148, threads = 128 * wps;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    fn<<<blocks, threads, 65536>>>(o, KTOT);
+    cudaEventRecord(e0);
+    for (int r = 0; r < 5; ++r) fn<<<blocks, threads, 65536>>>(o, KTOT);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double fl = 5.0 * blocks * threads * (double)KTOT * MP * NR * 4;
+    printf("ksg-NN shape %s %s warps/SMSP %d: %.1f TFLOP/s (%.3f of 73.5)  %s\n", DB ? "double-buffered" : "single",
+           RND ? "random data" : "i%7 data", wps,
+           fl / ms / 1e9, fl / ms / 1e9 / 73.5, cudaGetErrorString(cudaGetLastError()));
+}
+
 template <int ORDER, bool SMEM>
 void run(int wps, float *o)
 {
@@ -132,6 +208,12 @@ int main()
 {
     float *o;
     cudaMalloc(&o, 148 * 384 * 4);
+    for (int w = 2; w <= 3; ++w) {
+        run_ks<true, false>(w, o);
+        run_ks<false, false>(w, o);
+        run_ks<true, true>(w, o);
+        run_ks<false, true>(w, o);
+    }
     for (int w = 1; w <= 3; ++w) {
         run<0, true>(w, o);
         run<1, true>(w, o);

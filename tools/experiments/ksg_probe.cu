@@ -179,6 +179,9 @@ static void run(const Variant &v, int sms, float *dA, float *dB, float *dC, floa
     p.c_bytes = rup(p.c_tx, 1024);
     p.group_bytes = v.S * p.stage_bytes + p.c_bytes;
     p.beta_zero = 0;
+    p.C = reinterpret_cast<char *>(dC);  // C out through global (IAAT_KSG_C_STG)
+    p.ldc = M;
+    p.sC = (int64_t)M * N;
     const int BR = v.LR * v.MR, BC = (32 / v.LR) * v.NR;
     if (Mv % BR || Nv % BC) {
         printf("%s: block %dx%d does not divide %d\n", v.name.c_str(), BR, BC, n);
@@ -262,6 +265,15 @@ int main(int argc, char **argv)
         VD("NN80_10x10_l4_k16u2_g4w2_p1_s2_d2", false, false, 80, 80, 10, 10, 4, 16, 2, 4, 2, 1, 2, 2),
         VD("NN80_10x10_l4_k16u2_g4w2_p1_s2_d3", false, false, 80, 80, 10, 10, 4, 16, 2, 4, 2, 1, 2, 3),
         V("NN80_10x5_l4_k16u4_g3w4_p1_s3", false, false, 80, 80, 10, 5, 4, 16, 4, 3, 4, 1, 3),
+        V("NN80_10x10_l4_k16u1_g4w2_p1_s2", false, false, 80, 80, 10, 10, 4, 16, 1, 4, 2, 1, 2),
+        V("TT76_5x10_l8_k32u2_g2w4_p1_s3", true, true, 76, 80, 5, 10, 8, 32, 2, 2, 4, 1, 3),
+        V("TT80_10x10_l8_k16u2_g2w4_p2_s2", true, true, 80, 80, 10, 10, 8, 16, 2, 2, 4, 2, 2),
+        V("TT80_10x10_l8_k16u1_g2w4_p2_s2", true, true, 80, 80, 10, 10, 8, 16, 1, 2, 4, 2, 2),
+        V("TT80_10x10_l8_k16u2_g4w2_p1_s2", true, true, 80, 80, 10, 10, 8, 16, 2, 4, 2, 1, 2),
+        V("TT80_10x10_l8_k16u1_g4w2_p1_s2", true, true, 80, 80, 10, 10, 8, 16, 1, 4, 2, 1, 2),
+        VD("NN80_10x10_l4_k16u1_g4w2_p1_s2_d3", false, false, 80, 80, 10, 10, 4, 16, 1, 4, 2, 1, 2, 3),
+        V("NN80_10x5_l4_k16u2_g3w4_p1_s3", false, false, 80, 80, 10, 5, 4, 16, 2, 3, 4, 1, 3),
+        VD("NN80_10x5_l4_k16u2_g3w4_p1_s3_d3", false, false, 80, 80, 10, 5, 4, 16, 2, 3, 4, 1, 3, 3),
         VD("NN80_10x5_l4_k16u4_g3w4_p1_s3_d1", false, false, 80, 80, 10, 5, 4, 16, 4, 3, 4, 1, 3, 1),
         VD("NN80_10x5_l4_k16u4_g3w4_p1_s3_d2", false, false, 80, 80, 10, 5, 4, 16, 4, 3, 4, 1, 3, 2),
         VD("NN80_10x5_l4_k16u4_g3w4_p1_s3_d3", false, false, 80, 80, 10, 5, 4, 16, 4, 3, 4, 1, 3, 3),
