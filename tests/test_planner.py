@@ -210,7 +210,7 @@ def test_catalog_register_budget():
             # accumulators, lanes lr x 32/lr, two or three consumer warpgroups
             assert e["dtype"] == "f32" and e["trans"] != "TN"
             assert e["mr"] * e["nr"] <= 128 and 32 % e["lr"] == 0
-            assert e["g"] * e["w"] in (8, 12) and e["g"] <= 4 and e["kc"] in (16, 32) and e["ku"] in (2, 4)
+            assert e["g"] * e["w"] in (8, 12) and e["g"] <= 4 and e["kc"] in (16, 32) and e["ku"] in (1, 2, 4)
             assert tuple(e[k] for k in ("trans", "mr", "nr", "lr", "kc", "ku", "g", "w")) == gen.KSG_TILES[e["index"]]
         elif e["family"] == "ksgs":
             assert e["dtype"] == "f32" and e["mr"] * e["nr"] <= 100
@@ -299,11 +299,12 @@ def test_forced_k_streamed_plans_are_valid(fam):
         _forced()
 
 
-def test_fp64_default_is_k_streamed_dmma():
+def test_fp64_default_is_k_streamed_dmma(monkeypatch):
     """fp64 with M, N multiples of 8 and 16-byte aligned operands plans the
-    K-streamed DMMA kernels by default; warps = P x warp tiles, one warp tile
-    each; the MN-major pitch is 4 (mod 16) doubles (conflict-free fragment
-    rows)."""
+    K-streamed DMMA kernels by default (cost model, no install-time table);
+    warps = P x warp tiles, one warp tile each; the MN-major pitch is
+    4 (mod 16) doubles (conflict-free fragment rows)."""
+    monkeypatch.setenv("IAAT_NO_TUNING", "1")
     for tr in ("NN", "NT", "TT"):
         for n in (16, 32, 48, 64, 80):
             p = plan(1, tr, n, n, n, batch=200000, beta0=True)
