@@ -1,0 +1,17 @@
+# A/B: L2 prefetch of the first units before griddepcontrol.wait (pf) vs without (base), in the bench sequence
+set -x
+L=paper_2208_09822_b200
+cp $L/libiaat.so /tmp/libiaat_pf.so
+gunzip -c $L/libiaat_base.so.gz > /tmp/libiaat_base.so
+for r in 1 2; do
+for v in base pf; do
+  cp /tmp/libiaat_$v.so $L/libiaat.so
+  timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/g40_cfg2_${v}_$r.json 2> gpurun_out/g40_cfg2_${v}_$r.err
+  timeout 600 python bench.py --config 4 --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/g40_cfg4_${v}_$r.json 2> gpurun_out/g40_cfg4_${v}_$r.err
+done
+done
+cp /tmp/libiaat_pf.so $L/libiaat.so
+timeout 600 python bench.py --config 5 --steps 3 --warmup 1 --no-cpu --no-e2e > gpurun_out/g40_cfg5_pf.json 2> gpurun_out/g40_cfg5_pf.err
+for f in gpurun_out/g40_*.json; do python -c "
+import json,sys
+d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', d['value'], d['roofline']['kernel'], d['roofline']['frac'], d['clocks'])"; done
