@@ -327,9 +327,12 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     clocks.start()
     n_launch0 = iaat.iaat_launch_count()
+    # the timed region: K steps of back-to-back calls, events only at its
+    # two ends (an event between two calls would stand between the kernels
+    # in the stream and cost the programmatic-dependent-launch overlap)
     t0.record(stream)
     for k in range(args.steps):
-        step(evs[k])
+        step()
     t1.record(stream)
     torch.cuda.synchronize()
     n_launch = iaat.iaat_launch_count() - n_launch0
@@ -337,6 +340,12 @@ def run_ours(args, rank, world, local_rank):
     barrier(world)
     ms_total = t0.elapsed_time(t1)
     ms_total = allreduce_max(ms_total, world)
+    # per-call breakdown (roofline of the dominant launch, per-shape
+    # fractions): a second, instrumented pass of K steps with an event pair
+    # around every call -- not part of the timed value
+    for k in range(args.steps):
+        step(evs[k])
+    torch.cuda.synchronize()
     per_call_ms = np.zeros(len(chunks))
     for k in range(args.steps):
         for i, (a, b) in enumerate(evs[k]):
@@ -363,7 +372,7 @@ def run_ours(args, rank, world, local_rank):
     tdom = per_call_ms[dom] * 1e-3
     roof = roofline_of(s, cnt, tdom, pk)
     roof["kernel"] = s.name()
-    roof["share_of_step"] = round(per_call_ms[dom] / ms_step, 4)
+    roof["share_of_step"] = round(per_call_ms[dom] / per_call_ms.sum(), 4)
     roof["bytes_per_launch"] = s.alg_bytes(cnt)
     roof["flops_per_launch"] = s.flops(cnt)
 
@@ -379,7 +388,9 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": desc, "calls_per_step": len(chunks),
                        "l2": "inputs larger than L2: every call streams its own 256 MiB operand set "
                              "(126 MB L2), no flush kernel needed" if args.config == 2 else
-                             "as workload states", "parallelism": "dp%d (batch shards, no collective)" % world},
+                             "as workload states", "parallelism": "dp%d (batch shards, no collective)" % world,
+                       "timing": "K steps back to back, CUDA events at the two ends only; per-shape times "
+                                 "and the roofline launch from a second pass with an event pair per call"},
             "roofline": roof, "gpu_launches": int(n_launch), "clocks": clk, "e2e": e2e,
             "shapes": shapes_out}
     if args.config == 1:
