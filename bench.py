@@ -341,30 +341,16 @@ def run_ours(args, rank, world, local_rank):
     ms_total = t0.elapsed_time(t1)
     ms_total = allreduce_max(ms_total, world)
     # per-call breakdown (roofline of the dominant launch, per-shape
-    # fractions), not part of the timed value: each call of the step run K
-    # times back to back between one event pair (the calls keep their
-    # programmatic-dependent-launch overlap, as in the timed sequence; an
-    # event pair around every single call would add its launch gap to it).
-    # The instrumented sequence (an event pair per call) is reported beside
-    # it as "per_call_sequence_ms".
-    per_call_ms = np.zeros(len(chunks))
-    e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for i, (s, lo, cnt) in enumerate(chunks):
-        call(s, lo, cnt)
-        e_a.record(stream)
-        for _ in range(args.steps):
-            call(s, lo, cnt)
-        e_b.record(stream)
-        torch.cuda.synchronize()
-        per_call_ms[i] = e_a.elapsed_time(e_b) / args.steps
+    # fractions): a second, instrumented pass of K steps with an event pair
+    # around every call -- not part of the timed value
     for k in range(args.steps):
         step(evs[k])
     torch.cuda.synchronize()
-    seq_ms = np.zeros(len(chunks))
+    per_call_ms = np.zeros(len(chunks))
     for k in range(args.steps):
         for i, (a, b) in enumerate(evs[k]):
-            seq_ms[i] += a.elapsed_time(b)
-    seq_ms /= args.steps
+            per_call_ms[i] += a.elapsed_time(b)
+    per_call_ms /= args.steps
 
     flops_step = sum(s.flops(cnt) for s, lo, cnt in chunks)
     ms_step = ms_total / args.steps
@@ -381,8 +367,7 @@ def run_ours(args, rank, world, local_rank):
                      s.alg_bytes(cnt) / (pk["hbm_gbs"] * 1e9))
         shapes_out.append({"shape": s.name(), "batch": cnt, "us": round(t * 1e6, 2), "gflops": round(gf, 1),
                            "hbm_gbs": round(s.alg_bytes(cnt) / t / 1e9, 1),
-                           "frac_roofline": round(t_roof / t, 4),
-                           "us_in_sequence": round(seq_ms[i] * 1e3, 2)})
+                           "frac_roofline": round(t_roof / t, 4)})
     s, lo, cnt = chunks[dom]
     tdom = per_call_ms[dom] * 1e-3
     roof = roofline_of(s, cnt, tdom, pk)
@@ -405,9 +390,7 @@ def run_ours(args, rank, world, local_rank):
                              "(126 MB L2), no flush kernel needed" if args.config == 2 else
                              "as workload states", "parallelism": "dp%d (batch shards, no collective)" % world,
                        "timing": "K steps back to back, CUDA events at the two ends only; per-shape times "
-                                 "and the roofline launch: each call K times back to back between one event pair",
-                       "per_call_sum_ms": round(float(per_call_ms.sum()), 4),
-                       "per_call_sequence_sum_ms": round(float(seq_ms.sum()), 4)},
+                                 "and the roofline launch from a second pass with an event pair per call"},
             "roofline": roof, "gpu_launches": int(n_launch), "clocks": clk, "e2e": e2e,
             "shapes": shapes_out}
     if args.config == 1:
