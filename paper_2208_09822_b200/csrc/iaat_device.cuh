@@ -283,6 +283,101 @@ struct RegTile<float, MR, NR, 2> {  // pairs (j, j+1)
     }
 };
 
+template <int MR, int NR>
+struct RegTile<float, MR, NR, 3> {  // odd MR: pairs (i, i+1) for i < MR - 1, the last row scalar
+    unsigned long long v[MR / 2][NR];
+    float t[NR];
+    __device__ __forceinline__ void zero()
+    {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+#pragma unroll
+            for (int i = 0; i < MR / 2; ++i) v[i][j] = 0ull;
+            t[j] = 0.f;
+        }
+    }
+    template <typename AF, typename BF>
+    __device__ __forceinline__ void rank1(const AF &a, const BF &b)
+    {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+            const float bj = b(j);
+            const unsigned long long bb = pack_f32x2(bj, bj);
+#pragma unroll
+            for (int i = 0; i < MR / 2; ++i) ffma2(v[i][j], pack_f32x2(a(2 * i), a(2 * i + 1)), bb);
+            t[j] = fma_rn(a(MR - 1), bj, t[j]);
+        }
+    }
+    __device__ __forceinline__ void get(float (&o)[MR][NR]) const
+    {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+#pragma unroll
+            for (int i = 0; i < MR / 2; ++i) unpack_f32x2(v[i][j], o[2 * i][j], o[2 * i + 1][j]);
+            o[MR - 1][j] = t[j];
+        }
+    }
+};
+
+template <int MR, int NR>
+struct RegTile<float, MR, NR, 4> {  // odd NR: pairs (j, j+1) for j < NR - 1, the last column scalar
+    unsigned long long v[MR][NR / 2];
+    float t[MR];
+    __device__ __forceinline__ void zero()
+    {
+#pragma unroll
+        for (int i = 0; i < MR; ++i) {
+#pragma unroll
+            for (int j = 0; j < NR / 2; ++j) v[i][j] = 0ull;
+            t[i] = 0.f;
+        }
+    }
+    template <typename AF, typename BF>
+    __device__ __forceinline__ void rank1(const AF &a, const BF &b)
+    {
+#pragma unroll
+        for (int j = 0; j < NR / 2; ++j) {
+            const unsigned long long bb = pack_f32x2(b(2 * j), b(2 * j + 1));
+#pragma unroll
+            for (int i = 0; i < MR; ++i) ffma2(v[i][j], pack_f32x2(a(i), a(i)), bb);
+        }
+#pragma unroll
+        for (int i = 0; i < MR; ++i) t[i] = fma_rn(a(i), b(NR - 1), t[i]);
+    }
+    __device__ __forceinline__ void get(float (&o)[MR][NR]) const
+    {
+#pragma unroll
+        for (int i = 0; i < MR; ++i) {
+#pragma unroll
+            for (int j = 0; j < NR / 2; ++j) unpack_f32x2(v[i][j], o[i][2 * j], o[i][2 * j + 1]);
+            o[i][NR - 1] = t[i];
+        }
+    }
+};
+
+// Element (i, j) of a register tile, i and j compile-time after unrolling
+// (a pair's unpack is a register rename).
+template <int MR, int NR, int PAIR>
+__device__ __forceinline__ float tile_at(const RegTile<float, MR, NR, PAIR> &t, int i, int j)
+{
+    float lo, hi;
+    if constexpr (PAIR == 0) {
+        return t.v[i][j];
+    } else if constexpr (PAIR == 1 || PAIR == 3) {
+        if constexpr (PAIR == 3) {
+            if (i == MR - 1) return t.t[j];
+        }
+        unpack_f32x2(t.v[i / 2][j], lo, hi);
+        return (i & 1) ? hi : lo;
+    } else {
+        if constexpr (PAIR == 4) {
+            if (j == NR - 1) return t.t[i];
+        }
+        unpack_f32x2(t.v[i][j / 2], lo, hi);
+        return (j & 1) ? hi : lo;
+    }
+}
+
 // Pairing choice: along the dimension whose fragment arrives as consecutive
 // registers (contiguous in smem); fp64 and odd tiles use scalar FMAs.
 template <typename T, bool A_CONTIG, bool B_CONTIG, int MR, int NR>

@@ -567,14 +567,57 @@ template <bool TA, bool TB, int MR, int NR, int LR>
 struct GeoS {
     static constexpr int LC = 32 / LR;
     static constexpr bool AK = TA, BK = !TB;
-    // FFMA2 pairs along the MN-major operand (scalar loads: any two registers pair)
-    static constexpr int PAIR = (!AK && MR % 2 == 0) ? 1 : ((!BK && NR % 2 == 0) ? 2 : 0);
+    // FFMA2 pairs: scalar loads put any two values in a register pair, so
+    // either operand can supply the pairs -- the MN-major one when it can
+    // (3 / 4: odd MR / NR, pairs for all but the last row / column)
+    static constexpr int PAIR = (!AK && MR % 2 == 0) ? 1
+                              : (!BK && NR % 2 == 0) ? 2
+                              : (MR % 2 == 0) ? 1
+                              : (NR % 2 == 0) ? 2
+                              : (MR >= 3 && !AK) ? 3
+                              : (NR >= 3) ? 4
+                              : (MR >= 3) ? 3 : 0;
     static constexpr int BR = LR * MR, BC = LC * NR;
     __device__ static __forceinline__ int row(int ti, int r) { return ti + LR * r; }
     __device__ static __forceinline__ int col(int tj, int c) { return tj + LC * c; }
 };
 
-template <bool TA, bool TB, int MR, int NR, int LR, int G, int W>
+// Shared-memory map of ksgs: [full[S] | empty[S] barriers (1 KB)], then the
+// ring of S stages [A span | B span] shared by all groups.
+// ticket[s] = the unit sequence number j whose fill of stage s the producer
+// has started (written after it saw the stage's previous fill consumed).
+// Consecutive fills of a stage can belong to different groups, and an
+// mbarrier parity wait cannot tell fill n from fill n - 2: a group that
+// reached its wait for fill n while fill n - 1 was still pending would pass
+// at once.  A consumer therefore first waits for ticket[s] == j; from then
+// on the stage's barrier is in the phase of fill j / S.
+struct SmemS {
+    uint32_t ring, full, empty, ticket;
+    __device__ __forceinline__ explicit SmemS(unsigned char *smem)
+    {
+        const uint32_t sbase = smem_u32(smem);
+        ring = (sbase + IAAT_KSG_BAR_BYTES + 1023u) & ~1023u;
+        full = sbase;
+        empty = sbase + IAAT_KSGS_MAX_STAGES * 8;
+        ticket = sbase + IAAT_KSGS_MAX_STAGES * 16;
+    }
+};
+
+__device__ __forceinline__ void ticket_set(uint32_t a, int v)
+{
+    asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void ticket_wait(uint32_t a, int v)
+{
+    int t;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(t) : "r"(a) : "memory");
+    while (t != v) {  // rare: the stage still holds an earlier unit; back off, leave the SMSP to the others
+        __nanosleep(64);
+        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(t) : "r"(a) : "memory");
+    }
+}
+
+template <bool TA, bool TB, int MR, int NR, int LR, int G, int W, bool CS>
 __device__ __forceinline__ void ksgs_consumer(const IaatKsgParams &p, unsigned char *smem, int g, int w, int lane)
 {
     typedef GeoS<TA, TB, MR, NR, LR> Gm;
@@ -584,7 +627,7 @@ __device__ __forceinline__ void ksgs_consumer(const IaatKsgParams &p, unsigned c
     const int ti = lane % LR, tj = lane / LR;
     const int pl = w / p.wpp, blk = w - pl * p.wpp;
     const int R0 = (blk % p.bm) * Gm::BR, C0 = (blk / p.bm) * Gm::BC;
-    const Smem sm(smem, p, g);
+    const SmemS sm(smem);
     const float alpha = (float)p.alpha, beta = (float)p.beta;
     const bool beta_zero = p.beta_zero != 0;
     // element offsets (words) of the lane's rows / columns inside its problem
@@ -605,12 +648,16 @@ __device__ __forceinline__ void ksgs_consumer(const IaatKsgParams &p, unsigned c
     }
     const int64_t sA = p.sA, sB = p.sB, sC = p.sC;
 
-    int s = 0;
-    uint32_t phase = 0;
-    for (int64_t u = (int64_t)blockIdx.x * G + g; u < nunits; u += (int64_t)gridDim.x * G) {
+    // one ring of S stages shared by the G groups: the CTA's j-th unit
+    // (j = 0, 1, ...; group j % G) sits in stage j % S, fill j / S
+    int j = g;
+    for (int64_t u = (int64_t)blockIdx.x * G + g; u < nunits; u += (int64_t)gridDim.x * G, j += G) {
+        const int s = j % S;
+        const uint32_t phase = (uint32_t)(j / S) & 1u;
         const int64_t b0 = u * p.P, b = b0 + pl;
         RegTile<float, MR, NR, Gm::PAIR> acc;
         acc.zero();
+        ticket_wait(sm.ticket + 4 * s, j);
         bar_wait(sm.full + 8 * s, phase);
         {
             // the unit's spans start at these byte offsets inside the stage
@@ -634,12 +681,35 @@ __device__ __forceinline__ void ksgs_consumer(const IaatKsgParams &p, unsigned c
                 acc.rank1([&](int i) { return a[i]; }, [&](int j) { return bv[j]; });
             }
         }
+        if (CS) {
+            // fused epilogue in the stage's C span (C_in bulk-loaded with A
+            // and B when beta != 0; the producer bulk-stores the span once
+            // the group releases the stage)
+            if (b < batch) {
+                const uint32_t st = sm.ring + (uint32_t)(s * p.stage_bytes);
+                const uint32_t misC = (uint32_t)(reinterpret_cast<uintptr_t>(p.C + b0 * sC * 4) & 15u);
+                const uint32_t pc = st + (uint32_t)(p.a_bytes + p.b_bytes) + misC + (uint32_t)(pl * sC * 4);
+#pragma unroll
+                for (int c = 0; c < NR; ++c) {
+                    const int col = C0 + Gm::col(tj, c);
+#pragma unroll
+                    for (int r = 0; r < MR; ++r) {
+                        const int row = R0 + Gm::row(ti, r);
+                        if (row < M && col < N) {
+                            const uint32_t q = pc + (uint32_t)((col * ldc + row) * 4);
+                            const float x = tile_at(acc, r, c);
+                            sts32(q, beta_zero ? mul_rn(alpha, x) : fma_rn(alpha, x, mul_rn(beta, lds32(q))));
+                        }
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            __syncwarp();
+            if (lane == 0) bar_arrive(sm.empty + 8 * s);
+            continue;
+        }
         __syncwarp();
         if (lane == 0) bar_arrive(sm.empty + 8 * s);
-        if (++s == S) {
-            s = 0;
-            phase ^= 1u;
-        }
         if (b >= batch) continue;
         // fused epilogue, C through global: the C_in loads of a batch of
         // columns (<= 32 values) all issued before the batch's stores
@@ -687,18 +757,43 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_
         : "memory");
 }
 
-// Producer (slab staging): lane 0 of warp g, one stage per unit.
+// Producer (slab staging): one thread streams the CTA's units in order
+// j = 0, 1, ... (unit blockIdx.x * G + j % G + (j / G) * gridDim.x * G, the
+// unit group j % G consumes) into the shared ring, stage j % S.
 template <bool TA, bool TB, int G>
-__device__ __forceinline__ void ksgs_producer(const IaatKsgParams &p, unsigned char *smem, int g, int lane)
+__device__ __forceinline__ void ksgs_producer(const IaatKsgParams &p, unsigned char *smem)
 {
-    if (lane != 0) return;
     const uint64_t pol = policy_evict_first();
-    const Smem sm(smem, p, g);
+    const SmemS sm(smem);
     const int64_t colsA = TA ? p.M : p.K, rowsA = TA ? p.K : p.M;
     const int64_t colsB = TB ? p.K : p.N, rowsB = TB ? p.N : p.K;
-    int s = 0, it = 0;
-    uint32_t phase = 0;
-    for (int64_t u = (int64_t)blockIdx.x * G + g; u < p.nunits; u += (int64_t)gridDim.x * G, ++it) {
+    const int S = p.S;
+    // C span of the unit with sequence number j: elements [b0 * sC, (b0 + np) * sC)
+    // (c_bytes != 0 only for ldc == M and packed problems: gap-free).  The
+    // stage's C region holds it from its 16-byte-aligned start; the aligned
+    // interior leaves by one bulk store, the <= 3 + 3 elements in the
+    // granules shared with the neighbouring problems by plain stores.
+    auto store_c = [&](int j, uint32_t creg) {
+        const int64_t u = (int64_t)blockIdx.x * G + j % G + (int64_t)(j / G) * gridDim.x * G;
+        const int64_t b0 = u * p.P;
+        const int np = (int)min((int64_t)p.P, p.batch - b0);
+        const uintptr_t a = reinterpret_cast<uintptr_t>(p.C + b0 * p.sC * 4);
+        const uintptr_t e = a + (uintptr_t)((int64_t)np * p.sC * 4);
+        const uintptr_t lo = a & ~(uintptr_t)15;
+        const uintptr_t i0 = min((a + 15) & ~(uintptr_t)15, e), i1 = max(e & ~(uintptr_t)15, i0);
+        for (uintptr_t x = a; x < i0; x += 4) stg_cs(reinterpret_cast<float *>(x), lds32(creg + (uint32_t)(x - lo)));
+        for (uintptr_t x = i1; x < e; x += 4) stg_cs(reinterpret_cast<float *>(x), lds32(creg + (uint32_t)(x - lo)));
+        if (i1 > i0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(i0),
+                         "r"(creg + (uint32_t)(i0 - lo)), "r"((uint32_t)(i1 - i0))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    };
+    int jn = 0;
+    for (int j = 0;; ++j) {
+        const int64_t u = (int64_t)blockIdx.x * G + j % G + (int64_t)(j / G) * gridDim.x * G;
+        if (u >= p.nunits) break;
         const int64_t b0 = u * p.P;
         const int np = (int)min((int64_t)p.P, p.batch - b0);
         // the 16-byte-aligned span enclosing the unit's bytes of one operand
@@ -713,35 +808,52 @@ __device__ __forceinline__ void ksgs_producer(const IaatKsgParams &p, unsigned c
         uintptr_t loA, loB;
         const uint32_t nA = span(p.A, b0, p.sA, np, rowsA, colsA, p.lda, loA);
         const uint32_t nB = span(p.B, b0, p.sB, np, rowsB, colsB, p.ldb, loB);
-        if (it >= p.S) bar_wait(sm.empty + 8 * s, phase);
+        const int s = j % S;
+        if (j >= S) bar_wait(sm.empty + 8 * s, (uint32_t)(j / S - 1) & 1u);
         const uint32_t st = sm.ring + (uint32_t)(s * p.stage_bytes), fb = sm.full + 8 * s;
-        bar_expect_tx(fb, nA + nB);
+        if (p.c_bytes && j >= S) store_c(j - S, st + (uint32_t)(p.a_bytes + p.b_bytes));
+        ticket_set(sm.ticket + 4 * s, j);
+        uintptr_t loC = 0;
+        const uint32_t nC = p.beta_zero ? 0u : span(p.C, b0, p.sC, np, p.M, p.N, p.ldc, loC);
+        bar_expect_tx(fb, nA + nB + (p.c_bytes ? nC : 0u));
         bulk_load(st, reinterpret_cast<const void *>(loA), nA, fb, pol);
         bulk_load(st + (uint32_t)p.a_bytes, reinterpret_cast<const void *>(loB), nB, fb, pol);
-        if (!p.beta_zero) {
-            uintptr_t loC;
-            const uint32_t nC = span(p.C, b0, p.sC, np, p.M, p.N, p.ldc, loC);
+        if (p.c_bytes) {
+            if (nC) {
+                // the span store of the stage's previous unit must have read
+                // its C region before C_in lands there
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                bulk_load(st + (uint32_t)(p.a_bytes + p.b_bytes), reinterpret_cast<const void *>(loC), nC, fb, pol);
+            }
+        } else if (nC) {
             bulk_prefetch_l2(reinterpret_cast<const void *>(loC), nC);
         }
-        if (++s == p.S) {
-            s = 0;
-            if (it >= 2 * p.S - 1) phase ^= 1u;
+        ++jn;
+    }
+    if (p.c_bytes) {
+        // the last S units: store each C span once its group is done
+        for (int j = max(0, jn - S); j < jn; ++j) {
+            const int s = j % S;
+            bar_wait(sm.empty + 8 * s, (uint32_t)(j / S) & 1u);
+            store_c(j, sm.ring + (uint32_t)(s * p.stage_bytes + p.a_bytes + p.b_bytes));
         }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
 }
 
-template <bool TA, bool TB, int MR, int NR, int LR, int G, int W>
+// CS: C through the stage (p.c_bytes != 0; the launcher picks the instance)
+template <bool TA, bool TB, int MR, int NR, int LR, int G, int W, bool CS>
 __device__ __forceinline__ void ksgs_body(const IaatKsgParams &p)
 {
     static_assert(G * W == 8 || G * W == 12, "ksgs: two or three warpgroups of consumers");
-    static_assert(G <= IAAT_KSG_MAX_GROUPS, "ksgs: barrier area holds IAAT_KSG_MAX_GROUPS groups");
     extern __shared__ __align__(1024) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x < G) {
-        const Smem sm(smem, p, threadIdx.x);
+    if (threadIdx.x == 0) {
+        const SmemS sm(smem);
         for (int s = 0; s < p.S; ++s) {
             bar_init(sm.full + 8 * s, 1);
             bar_init(sm.empty + 8 * s, W);
+            ticket_set(sm.ticket + 4 * s, -1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -750,11 +862,11 @@ __device__ __forceinline__ void ksgs_body(const IaatKsgParams &p)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp < 4) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(IAAT_KSG_PRODUCER_REGS));
-        if (warp < G) ksgs_producer<TA, TB, G>(p, smem, warp, lane);
+        if (threadIdx.x == 0) ksgs_producer<TA, TB, G>(p, smem);
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(IAAT_KSG_CONSUMER_REGS_OF(G * W)));
         const int c = warp - 4;
-        ksgs_consumer<TA, TB, MR, NR, LR, G, W>(p, smem, c / W, c % W, lane);
+        ksgs_consumer<TA, TB, MR, NR, LR, G, W, CS>(p, smem, c / W, c % W, lane);
     }
 }
 

@@ -134,6 +134,7 @@ struct IaatKsParams {
 #define IAAT_KSG_MAX_GROUPS 4
 #define IAAT_KSG_GROUP_BARS (2 * IAAT_KSG_MAX_STAGES + 2)  // full[S], empty[S], cfull, cready
 #define IAAT_KSG_BAR_BYTES 1024
+#define IAAT_KSGS_MAX_STAGES 32  // ksgs: one shared ring; full[], empty[], ticket[] in the 1 KB barrier area
 
 struct IaatKsgParams {
     int64_t batch;
@@ -141,7 +142,7 @@ struct IaatKsgParams {
     double alpha, beta;
     int M, N, K;           // the problem
     int Mv, Nv;            // the tiled (virtual) extent: Mv - M, Nv - N rows / columns of zero fill
-    int P, S, nchunks;     // problems per unit, stages per group ring, ceil(K / KC)
+    int P, S, nchunks;     // problems per unit, stages per group ring (ksgs: of the one shared ring), ceil(K / KC)
     int a_pitch, b_pitch;  // MN-major operands: smem row pitch (elements) = TMA box inner dim
     int c_pitch;           // C buffer: elements per column (TMA box inner dim >= Mv; padded against bank conflicts)
     int a_bytes, b_bytes;  // smem bytes of one stage's A / B region (multiples of 1024)

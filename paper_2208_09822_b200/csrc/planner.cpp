@@ -577,7 +577,7 @@ bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
     pl.ctas = 1;
     pl.grid = (int)std::min<int64_t>((k.nunits + e.g - 1) / e.g, (int64_t)r.sm_count);
     pl.block = 128 + 32 * e.g * e.w;  // IAAT_KSG_THREADS_OF(g * w): producer warpgroup + consumers
-    pl.smem = IAAT_KSG_BAR_BYTES + 1024 + e.g * k.group_bytes;
+    pl.smem = IAAT_KSG_BAR_BYTES + 1024 + k.group_bytes;
     pl.est_total = best.cost;
     // the paper's cost over the Mv x Nv tiling: smem words
     // the lanes' tiles read per k-step, plus the C traffic
@@ -608,11 +608,16 @@ bool plan_ksgs(const PlanRequest &r, const Knobs &kn, Plan &out)
     const int tidx = r.transA * 2 + r.transB;
     const int nent = (int)(sizeof(kKsgsCatalog) / sizeof(kKsgsCatalog[0]));
     struct Cand {
-        int idx = -1, Mv = 0, Nv = 0, P = 0, S = 0, bm = 0, wpp = 0, ab = 0, bb = 0;
+        int idx = -1, Mv = 0, Nv = 0, P = 0, S = 0, bm = 0, wpp = 0, ab = 0, bb = 0, cb = 0;
         double cost = 0;
     } best;
     const double bytes = (double)(M * K + K * N + M * N * (r.beta_zero ? 1 : 2)) * elt;
     const int64_t sA = r.batch > 1 ? r.sA : r.lda * colsA, sB = r.batch > 1 ? r.sB : r.ldb * colsB;
+    // C through the stage (C_in bulk-loaded with A and B, C bulk-stored by the
+    // producer): only where a unit's C is one gap-free span (ldc == M, packed
+    // problems), so that the span store writes nothing but C elements
+    const bool cpack = r.ldc == M && (r.batch <= 1 || r.sC == M * N);
+    const bool csm = cpack && !(kn.fam == IAAT_FAM_KSGS && kn.csmem == 0);
     for (int i = 0; i < nent; ++i) {
         const IaatKsgsCatalogEntry &e = kKsgsCatalog[i];
         if (e.trans != tidx) continue;
@@ -628,18 +633,24 @@ bool plan_ksgs(const PlanRequest &r, const Knobs &kn, Plan &out)
         const int64_t slackA = (AK ? (int64_t)(Mv - M) * r.lda : (Mv - M)) * elt;
         const int64_t slackB = (BK ? (int64_t)(Nv - N) * r.ldb : (Nv - N)) * elt;
         const int ab = (int)round_up(spanA + 32 + slackA, 128), bb = (int)round_up(spanB + 32 + slackB, 128);
-        const int stage = ab + bb;
+        // (no CS instance for 10 x 10 tiles: gen/generate.py ksgs_cs)
+        const int cb = csm && e.mr * e.nr < 100 ? (int)round_up((int64_t)P * M * N * elt + 32, 128) : 0;
+        const int stage = ab + bb + cb;
+        // one ring of S stages shared by the e.g groups (csrc/iaat_ksg.cuh SmemS)
         int S = 0;
-        while (S < IAAT_KSG_MAX_STAGES && IAAT_KSG_BAR_BYTES + 1024 + e.g * (S + 1) * stage <= IAAT_SMEM_LIMIT) ++S;
+        while (S < IAAT_KSGS_MAX_STAGES && IAAT_KSG_BAR_BYTES + 1024 + (S + 1) * stage <= IAAT_SMEM_LIMIT) ++S;
         if (kn.fam == IAAT_FAM_KSGS && kn.s > 0) S = std::min(S, kn.s);
         if (S < 1) continue;
+        // units in flight beyond the G being computed: the loads they hide
+        const int ahead = S - e.g;
         // scalar loads: (mr + nr) LDS per k-step beside mr*nr/2 FFMA2
-        const bool pair = (!AK && e.mr % 2 == 0) || (!BK && e.nr % 2 == 0);
-        const double fma = (double)P * Mv * Nv * K / (128.0 * (pair ? 0.6 : 0.45)) / P;
+        const bool pair = e.mr % 2 == 0 || e.nr % 2 == 0;  // odd x odd: all but one row / column paired
+        const double fma = (double)P * Mv * Nv * K / (128.0 * (pair ? 0.6 : 0.55)) / P;
         const double smemf = 4.0 * (e.mr + e.nr) / (e.mr * e.nr);
         const double hbm = bytes / 22.0;
         double t = std::max(fma * std::max(1.0, smemf / 0.9), hbm) + 0.35 * std::min(fma, hbm);
-        if (S == 1) t *= 1.25;
+        if (ahead < 1) t *= 1.6;
+        else if (ahead < 2) t *= 1.15;
         if (best.idx < 0 || t < best.cost) {
             best.idx = i;
             best.Mv = Mv;
@@ -650,6 +661,7 @@ bool plan_ksgs(const PlanRequest &r, const Knobs &kn, Plan &out)
             best.wpp = wpp;
             best.ab = ab;
             best.bb = bb;
+            best.cb = cb;
             best.cost = t;
         }
     }
@@ -669,8 +681,8 @@ bool plan_ksgs(const PlanRequest &r, const Knobs &kn, Plan &out)
     k.nchunks = 1;
     k.a_bytes = best.ab;
     k.b_bytes = best.bb;
-    k.stage_bytes = best.ab + best.bb;
-    k.c_bytes = 0;
+    k.stage_bytes = best.ab + best.bb + best.cb;
+    k.c_bytes = best.cb;  // 0: C through global
     k.group_bytes = best.S * k.stage_bytes;
     k.beta_zero = r.beta_zero;
     k.bm = best.bm;
@@ -688,7 +700,7 @@ bool plan_ksgs(const PlanRequest &r, const Knobs &kn, Plan &out)
     pl.ctas = 1;
     pl.grid = (int)std::min<int64_t>((k.nunits + e.g - 1) / e.g, (int64_t)r.sm_count);
     pl.block = 128 + 32 * e.g * e.w;
-    pl.smem = IAAT_KSG_BAR_BYTES + 1024 + e.g * k.group_bytes;
+    pl.smem = IAAT_KSG_BAR_BYTES + 1024 + k.group_bytes;
     pl.est_total = best.cost;
     pl.memops = (int64_t)(best.Mv / e.mr) * (best.Nv / e.nr) * (e.mr + e.nr) * K + 2 * M * N;
     pl.status = 0;
@@ -1655,10 +1667,10 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
         const IaatKsgsCatalogEntry &e = kKsgsCatalog[p.kg_entry];
         add("\"family\": \"ksgs\", \"entry\": %d, \"mr\": %d, \"nr\": %d, \"lane_rows\": %d, \"groups\": %d, "
             "\"warps_per_group\": %d, \"Mv\": %d, \"Nv\": %d, \"P\": %d, \"S\": %d, \"a_bytes\": %d, "
-            "\"b_bytes\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, \"nunits\": %lld, \"est\": %.0f, "
-            "\"memops\": %lld, ",
-            p.kg_entry, e.mr, e.nr, e.lr, e.g, e.w, q.Mv, q.Nv, q.P, q.S, q.a_bytes, q.b_bytes, p.grid, p.block,
-            p.smem, (long long)q.nunits, p.est_total, (long long)p.memops);
+            "\"b_bytes\": %d, \"c_bytes\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, \"nunits\": %lld, "
+            "\"est\": %.0f, \"memops\": %lld, ",
+            p.kg_entry, e.mr, e.nr, e.lr, e.g, e.w, q.Mv, q.Nv, q.P, q.S, q.a_bytes, q.b_bytes, q.c_bytes, p.grid,
+            p.block, p.smem, (long long)q.nunits, p.est_total, (long long)p.memops);
         s += "\"classes\": []}";
         return s;
     }

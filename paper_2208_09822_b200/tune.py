@@ -362,6 +362,8 @@ def tune_ksg(sh, current, log):
         cands.append({"family": fam, "order": e["index"]})
         if p["S"] > 1:
             cands.append({"family": fam, "order": e["index"], "s": p["S"] - 1})
+        if fam == 8:  # ksgs: C through global instead of through the stage
+            cands.append({"family": fam, "order": e["index"], "csmem": 0})
     res = []
     for kw in cands:
         set_knobs(**kw)

@@ -26,7 +26,7 @@ F32 = np.float32
 
 def _force(**kw):
     for k in ("IAAT_FORCE_FAMILY", "IAAT_FORCE_TILE", "IAAT_FORCE_P", "IAAT_FORCE_CTAS", "IAAT_FORCE_ORDER",
-              "IAAT_FORCE_S"):
+              "IAAT_FORCE_S", "IAAT_FORCE_CSMEM"):
         os.environ.pop(k, None)
     for k, v in kw.items():
         os.environ["IAAT_FORCE_" + k.upper()] = str(v)
@@ -165,3 +165,46 @@ def test_ksgs_every_entry_odd_shapes_parity_and_bitwise_vs_slab(tr):
 def iaat_entries(fam):
     from paper_2208_09822_b200 import iaat
     return [e for e in iaat.iaat_catalog_describe() if e["family"] == fam]
+
+
+@pytest.mark.parametrize("tr", ["NN", "NT", "TT", "TN"])
+def test_ksgs_shared_ring_wraps(tr):
+    """ksgs's one ring of S stages shared by G groups (csrc/iaat_ksg.cuh
+    SmemS): a batch large enough that every CTA runs more than 2S units, so
+    every stage is refilled and both mbarrier phases recur; every entry
+    forced, the smallest and the largest S the planner allows (IAAT_FORCE_S),
+    sampled against the oracle, bitwise against the slab family; C through
+    the stage (span store by the producer) and through global (CSMEM=0)."""
+    ents = [e for e in iaat_entries("ksgs") if e["trans"] == tr]
+    shapes = [(37, 67, 79), (31, 37, 37), (79, 31, 53)] if tr != "TN" else [(31, 31, 31), (17, 23, 19)]
+    ran = 0
+    try:
+        for e in ents:
+            for (M, N, K) in shapes:
+                _force(family=8, order=e["index"])
+                probe = Case(F32, tr[0], tr[1], M, N, K, 1, 7, 1.0, 1.0)
+                p = _plan(probe, 1.0)
+                if p.get("family") != "ksgs" or p.get("entry") != e["index"]:
+                    continue
+                G, S = e["g"], p["S"]
+                for s, cs in sorted({(min(S, G + 1), 1), (S, 1), (S, 0)}):
+                    batch = 148 * G * p["P"] * (2 * s + 1) + 5  # + a ragged last unit
+                    _force(family=8, order=e["index"], s=s, **({} if cs else {"csmem": 0}))
+                    c = Case(F32, tr[0], tr[1], M, N, K, batch, 43, 1.25, -0.5)
+                    p2 = _plan(c, -0.5)
+                    assert p2.get("entry") == e["index"] and p2["S"] <= s, p2
+                    assert (p2["c_bytes"] > 0) == (cs == 1 and e["mr"] * e["nr"] < 100), p2
+                    c.run()
+                    torch.cuda.synchronize()
+                    c.check(sample_ids(c.batch, 64, 32))
+                    got = c.C.clone()
+                    _force(family=0)
+                    c2 = Case(F32, tr[0], tr[1], M, N, K, batch, 43, 1.25, -0.5)
+                    c2.run()
+                    torch.cuda.synchronize()
+                    assert bits_equal(got, c2.C), (tr, e, M, N, K, s)
+                    ran += 1
+                break
+    finally:
+        _force()
+    assert ran >= len(ents), ran
