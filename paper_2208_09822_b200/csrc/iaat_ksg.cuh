@@ -669,16 +669,41 @@ __device__ __forceinline__ void ksgs_consumer(const IaatKsgParams &p, unsigned c
             // k-step stride (bytes) of the MN-major operands
             const uint32_t ka = AK ? 4u : (uint32_t)lda * 4u, kb = BK ? 4u : (uint32_t)ldb * 4u;
             uint32_t xa = pa + (AK ? 0u : (uint32_t)oa[0] * 4u), xb = pb + (BK ? 0u : (uint32_t)ob[0] * 4u);
-#pragma unroll 4
-            for (int k = 0; k < K; ++k, xa += ka, xb += kb) {
-                float a[MR], bv[NR];
+            auto frag = [&](float (&a)[MR], float (&bv)[NR], uint32_t ya, uint32_t yb) {
 #pragma unroll
                 for (int r = 0; r < MR; ++r)
-                    a[r] = lds32(AK ? xa + (uint32_t)oa[r] * 4u : xa + (uint32_t)(LR * r * 4));
+                    a[r] = lds32(AK ? ya + (uint32_t)oa[r] * 4u : ya + (uint32_t)(LR * r * 4));
 #pragma unroll
                 for (int c = 0; c < NR; ++c)
-                    bv[c] = lds32(BK ? xb + (uint32_t)ob[c] * 4u : xb + (uint32_t)(Gm::LC * c * 4));
-                acc.rank1([&](int i) { return a[i]; }, [&](int j) { return bv[j]; });
+                    bv[c] = lds32(BK ? yb + (uint32_t)ob[c] * 4u : yb + (uint32_t)(Gm::LC * c * 4));
+            };
+            // register double buffering (the paper's ping-pang):
+            // k + 1's fragments load while k's FFMA2s issue -- for tiles of
+            // <= 72 accumulators (the larger ones would spill at the 168-
+            // register cap; they keep the plain unrolled loop)
+            if constexpr (MR * NR > 72) {
+#pragma unroll 4
+                for (int k = 0; k < K; ++k, xa += ka, xb += kb) {
+                    float a[MR], bv[NR];
+                    frag(a, bv, xa, xb);
+                    acc.rank1([&](int i) { return a[i]; }, [&](int j) { return bv[j]; });
+                }
+            } else {
+            float a0[MR], b0[NR], a1[MR], b1[NR];
+            frag(a0, b0, xa, xb);
+            int k = 0;
+#pragma unroll 2
+            for (; k + 2 <= K; k += 2) {
+                frag(a1, b1, xa + ka, xb + kb);
+                acc.rank1([&](int i) { return a0[i]; }, [&](int j) { return b0[j]; });
+                // k + 2 (clamped to the last k-step: a valid address, loaded and unused)
+                const uint32_t st2 = k + 2 < K ? 2u : 1u;
+                xa += st2 * ka;
+                xb += st2 * kb;
+                frag(a0, b0, xa, xb);
+                acc.rank1([&](int i) { return a1[i]; }, [&](int j) { return b1[j]; });
+            }
+            if (k < K) acc.rank1([&](int i) { return a0[i]; }, [&](int j) { return b0[j]; });
             }
         }
         if (CS) {

@@ -441,6 +441,12 @@ bool ksg_default(const PlanRequest &r)
            !(r.transA == 1 && r.transB == 0) && !std::getenv("IAAT_NO_KSG");
 }
 
+bool ksgs_default(const PlanRequest &r)
+{
+    return r.dtype == 0 && !r.ptr_array && std::min(r.M, r.N) >= 24 && r.K >= 8 &&
+           !(r.transA == 1 && r.transB == 0) && std::getenv("IAAT_KSGS_DEFAULT");
+}
+
 bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
 {
     if (r.ptr_array || r.dtype != 0) return false;
@@ -577,7 +583,7 @@ bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
     pl.ctas = 1;
     pl.grid = (int)std::min<int64_t>((k.nunits + e.g - 1) / e.g, (int64_t)r.sm_count);
     pl.block = 128 + 32 * e.g * e.w;  // IAAT_KSG_THREADS_OF(g * w): producer warpgroup + consumers
-    pl.smem = IAAT_KSG_BAR_BYTES + 1024 + k.group_bytes;
+    pl.smem = IAAT_KSG_BAR_BYTES + 1024 + e.g * k.group_bytes;
     pl.est_total = best.cost;
     // the paper's cost over the Mv x Nv tiling: smem words
     // the lanes' tiles read per k-step, plus the C traffic
@@ -772,6 +778,12 @@ Plan make_plan(const PlanRequest &r)
         // the slab family on average, profiles/r02/heldout_r02*.)
         Plan pg;
         if (plan_ksg(r, Knobs(), pg)) return pg;
+    }
+    if (!kn.any() && ksgs_default(r)) {
+        // the same upper half where the TMA rules fail (odd ld's, misaligned
+        // bases): the slab-staged lane grids
+        Plan pg;
+        if (plan_ksgs(r, Knobs(), pg)) return pg;
     }
     Plan p = make_plan_knobs(r, kn);
     if (p.status != 0 && kn.any()) p = make_plan_knobs(r, Knobs());

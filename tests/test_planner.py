@@ -49,6 +49,8 @@ def check_ksgs_plan(p, tr, M, N):
     assert M <= p["Mv"] < M + br and N <= p["Nv"] < N + bc
     assert (p["Mv"] // br) * (p["Nv"] // bc) * p["P"] == e["w"]
     assert p["smem"] <= 227 * 1024 and p["S"] >= 1
+    # one ring of S stages [A | B | C] shared by the groups, after the 1 KB barrier area
+    assert p["smem"] >= 2048 + p["S"] * (p["a_bytes"] + p["b_bytes"] + p["c_bytes"])
 
 
 def check_ksg_plan(p, tr, M, N):
@@ -67,6 +69,11 @@ def check_ksg_plan(p, tr, M, N):
     assert e["g"] * e["w"] in (8, 12) and p["block"] == 128 + 32 * e["g"] * e["w"]
     assert 1 <= p["S"] <= 8 and p["c_pitch"] >= p["Mv"] and p["c_pitch"] % 4 == 0
     assert p["smem"] <= 227 * 1024
+    # every group's ring (S stages of one A box and one B box) and C buffer fit
+    r1k = lambda x: -(-x // 1024) * 1024  # noqa: E731
+    P, kc = p["P"], e["kc"]
+    group = p["S"] * (r1k(P * p["Mv"] * kc * 4) + r1k(P * p["Nv"] * kc * 4)) + r1k(P * p["Nv"] * p["c_pitch"] * 4)
+    assert p["smem"] >= 2048 + e["g"] * group, (p, group)
     assert p["grid"] <= 148
 
 
