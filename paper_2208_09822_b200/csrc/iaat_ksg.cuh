@@ -101,14 +101,16 @@ __device__ __forceinline__ void sts128(uint32_t a, float x, float y, float z, fl
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
 }
 
-// Lane-grid geometry of one class.
-template <bool TA, bool TB, int MR, int NR, int LR>
+// Lane-grid geometry of one class.  PV (column-pair boxes, IaatKsgParams::
+// pairv): column pitches are 8-byte, not 16-byte, multiples, so MN-major
+// vector groups are at most 2 wide.
+template <bool TA, bool TB, int MR, int NR, int LR, bool PV = false>
 struct Geo {
     static constexpr int LC = 32 / LR;
     static constexpr bool AK = TA;   // op(A) K-major in smem
     static constexpr bool BK = !TB;  // op(B) K-major in smem
-    static constexpr int VA = AK ? 1 : (MR % 4 == 0 ? 4 : (MR % 2 == 0 ? 2 : 1));
-    static constexpr int VB = BK ? 1 : (NR % 4 == 0 ? 4 : (NR % 2 == 0 ? 2 : 1));
+    static constexpr int VA = AK ? 1 : ((MR % 4 == 0 && !PV) ? 4 : (MR % 2 == 0 ? 2 : 1));
+    static constexpr int VB = BK ? 1 : ((NR % 4 == 0 && !PV) ? 4 : (NR % 2 == 0 ? 2 : 1));
     // FFMA2 pairs along the dim whose fragments arrive as vectors
     static constexpr int PAIR = (!AK && VA >= 2) ? 1 : ((!BK && VB >= 2) ? 2 : 0);
     static constexpr int BR = LR * MR;  // warp block rows
@@ -135,15 +137,38 @@ __device__ __forceinline__ uint32_t kmaj_base(int ra)
 // row's base serves all rows and the rest are immediates (UNI): no per-row
 // LOP3 / IADD in the k loop (measured: the general path made NN / TT loops
 // ~9 % slower than NT's, which has no K-major operand).
-template <bool KMAJ, int R, int V, int L, int KC>
+// PV (column-pair boxes), K-major: the even and the odd columns of the
+// operand arrive as two unswizzled half boxes with rows of KC + 4 elements
+// (TMA box starts must be 16-byte aligned -- measured: an 8-byte-aligned
+// inner coordinate faults -- so the odd columns' box starts ld % 4 elements
+// early and their k values sit that far into the row).  A lane's rows all
+// have the parity of its first row: they sit L / 2 rows apart in one half
+// box, at immediates from base[0]; the 8-byte row offsets allow LDS.64, and
+// rows 20 / 36 words apart keep a quarter-warp's pairs in distinct banks.
+template <bool KMAJ, int R, int V, int L, int KC, bool PV = false>
 struct Opnd {
-    static constexpr bool UNI = KMAJ && (L % 8 == 0);
+    static constexpr bool UNI = KMAJ && (L % 8 == 0) && !PV;
+    static constexpr uint32_t PSTEP = (uint32_t)((L / 2) * (KC + 4) * 4);  // PV K-major: bytes between a lane's rows
     uint32_t base[KMAJ ? R : 1];  // K-major: per-row swizzled base; MN-major: first element
     uint32_t pitch;               // MN-major: bytes per k-step
     template <int KU>
     __device__ __forceinline__ void load(float (&f)[KU][R], uint32_t stage, int kb) const
     {
-        if (UNI) {
+        if (PV && KMAJ) {
+            const uint32_t x = stage + base[0] + (uint32_t)kb * 4u;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t a = x + (uint32_t)r * PSTEP;
+                if (KU == 4) {
+                    lds64(a, f[0][r], f[KU > 1 ? 1 : 0][r]);
+                    lds64(a + 8, f[KU > 2 ? 2 : 0][r], f[KU > 3 ? 3 : 0][r]);
+                } else if (KU == 2) {
+                    lds64(a, f[0][r], f[KU > 1 ? 1 : 0][r]);
+                } else {
+                    f[0][r] = lds32(a);
+                }
+            }
+        } else if (UNI) {
             const uint32_t q = (uint32_t)(kb >> 2) << 4, w = (uint32_t)(kb & 3) * 4u;
             const uint32_t x = stage + (base[0] ^ q) + (KU == 4 ? 0u : w);
 #pragma unroll
@@ -178,7 +203,10 @@ struct Opnd {
     // one k-step (ragged chunk tails)
     __device__ __forceinline__ void load1(float (&f)[R], uint32_t stage, int k) const
     {
-        if (KMAJ) {
+        if (PV && KMAJ) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) f[r] = lds32(stage + base[0] + (uint32_t)k * 4u + (uint32_t)r * PSTEP);
+        } else if (KMAJ) {
             const uint32_t q = (uint32_t)(k >> 2) << 4, w = (uint32_t)(k & 3) * 4u;
 #pragma unroll
             for (int r = 0; r < R; ++r) f[r] = lds32(stage + (base[r] ^ q) + w);
@@ -265,10 +293,10 @@ __device__ __forceinline__ void bar_wait(uint32_t b, uint32_t parity)
 // DBG (experiment builds only; the library instantiates DBG = 0):
 //   bit 0: no A/B staging (consumers never wait for or release stages),
 //   bit 1: no epilogue (no C load / update / store).
-template <bool TA, bool TB, int MR, int NR, int LR, int KC, int KU, int G, int W, int DBG = 0>
+template <bool TA, bool TB, int MR, int NR, int LR, int KC, int KU, int G, int W, int DBG = 0, bool PV = false>
 __device__ __forceinline__ void ksg_consumer(const IaatKsgParams &p, unsigned char *smem, int g, int w, int lane)
 {
-    typedef Geo<TA, TB, MR, NR, LR> Gm;
+    typedef Geo<TA, TB, MR, NR, LR, PV> Gm;
     constexpr bool AK = Gm::AK, BK = Gm::BK;
     const int K = p.K, nchunks = p.nchunks, S = p.S, Mv = p.Mv, Nv = p.Nv, cp = p.c_pitch;
     const int64_t nunits = p.nunits;
@@ -277,15 +305,24 @@ __device__ __forceinline__ void ksg_consumer(const IaatKsgParams &p, unsigned ch
     const int R0 = (blk % p.bm) * Gm::BR, C0 = (blk / p.bm) * Gm::BC;
     const Smem sm(smem, p, g);
 
-    Opnd<AK, MR, Gm::VA, LR, KC> oa;
-    Opnd<BK, NR, Gm::VB, Gm::LC, KC> ob;
-    if (AK) {
+    Opnd<AK, MR, Gm::VA, LR, KC, PV> oa;
+    Opnd<BK, NR, Gm::VB, Gm::LC, KC, PV> ob;
+    // PV: byte offset of K-major row / column x of problem pl -- even ones in
+    // the first half box, odd ones in the second, ld % 4 elements into the row
+    auto pvrow = [&](int x, int ext, int half, int ld) {
+        return (uint32_t)((x & 1) * (half + (ld & 3) * 4) + (pl * (ext >> 1) + (x >> 1)) * (KC + 4) * 4);
+    };
+    if (AK && PV) {
+        oa.base[0] = pvrow(R0 + Gm::row(ti, 0), Mv, p.a_half, p.lda);
+    } else if (AK) {
 #pragma unroll
         for (int r = 0; r < MR; ++r) oa.base[r] = kmaj_base<KC>(pl * Mv + R0 + Gm::row(ti, r));
     } else {
         oa.base[0] = (uint32_t)((pl * KC * p.a_pitch + R0 + Gm::VA * ti) * 4);
     }
-    if (BK) {
+    if (BK && PV) {
+        ob.base[0] = pvrow(C0 + Gm::col(tj, 0), Nv, p.b_half, p.ldb);
+    } else if (BK) {
 #pragma unroll
         for (int c = 0; c < NR; ++c) ob.base[c] = kmaj_base<KC>(pl * Nv + C0 + Gm::col(tj, c));
     } else {
@@ -297,6 +334,9 @@ __device__ __forceinline__ void ksg_consumer(const IaatKsgParams &p, unsigned ch
     const bool beta_zero = p.beta_zero != 0;
     // this warp block's first C element in the group's C buffer
     const uint32_t cb0 = sm.cbuf + (uint32_t)(((pl * Nv + C0) * cp + R0) * 4);
+    // PV: the C buffer's columns are M apart, so a row past M would land in
+    // the next column: the only boundary code, one predicate per store
+    const int mrows = PV ? p.M - R0 : (1 << 30);
 
     int s = 0;
     uint32_t phase = 0, cphase = 0;
@@ -375,6 +415,7 @@ __device__ __forceinline__ void ksg_consumer(const IaatKsgParams &p, unsigned ch
 #pragma unroll
                 for (int q = 0; q < MR / 2; ++q) {
                     const uint32_t a = colb + (uint32_t)(Gm::row(ti, 2 * q) * 4);
+                    if (PV && Gm::row(ti, 2 * q) >= mrows) continue;
                     unsigned long long o;
                     if (beta_zero) {
                         asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(o) : "l"(a2), "l"(acc.v[q][c]));
@@ -397,6 +438,7 @@ __device__ __forceinline__ void ksg_consumer(const IaatKsgParams &p, unsigned ch
 #pragma unroll
                     for (int g4 = 0; g4 < MR / Gm::VA; ++g4) {
                         const uint32_t q = colb + (uint32_t)(Gm::row(ti, Gm::VA * g4) * 4);
+                        if (PV && Gm::row(ti, Gm::VA * g4) >= mrows) continue;
                         float ci[4] = {0.f, 0.f, 0.f, 0.f}, o[4];
                         if (!beta_zero) {
                             if (Gm::VA == 4) lds128(q, ci[0], ci[1], ci[2], ci[3]);
@@ -414,6 +456,7 @@ __device__ __forceinline__ void ksg_consumer(const IaatKsgParams &p, unsigned ch
 #pragma unroll
                     for (int r = 0; r < MR; ++r) {
                         const uint32_t q = colb + (uint32_t)(Gm::row(ti, r) * 4);
+                        if (PV && Gm::row(ti, r) >= mrows) continue;
                         const float x = v[r][c];
                         sts32(q, beta_zero ? mul_rn(alpha, x) : fma_rn(alpha, x, mul_rn(beta, lds32(q))));
                     }
@@ -429,7 +472,7 @@ __device__ __forceinline__ void ksg_consumer(const IaatKsgParams &p, unsigned ch
 // Producer warp of group g: lane 0 streams the group's units chunk by chunk,
 // and after each unit's chunks are queued it retires the previous unit's C
 // (TMA store once its epilogue is done) and brings in this unit's C_in.
-template <bool TA, bool TB, int KC, int G, int DBG = 0>
+template <bool TA, bool TB, int KC, int G, int DBG = 0, bool PV = false>
 __device__ __forceinline__ void ksg_producer(const IaatKsgParams &p, const CUtensorMap *tmA, const CUtensorMap *tmB,
                                              const CUtensorMap *tmC, unsigned char *smem, int g, int lane)
 {
@@ -460,10 +503,29 @@ __device__ __forceinline__ void ksg_producer(const IaatKsgParams &p, const CUten
         const uint32_t st = sm.ring + (uint32_t)(s * p.stage_bytes), fb = sm.full + 8 * s;
         bar_expect_tx(fb, tx);
         const int k0 = c * KC;
-        if (TA) tma_load_3d(st, tmA, k0, 0, b0, fb, polA);
-        else tma_load_3d(st, tmA, 0, k0, b0, fb, polA);
-        if (TB) tma_load_3d(st + p.a_bytes, tmB, 0, k0, b0, fb, polB);
-        else tma_load_3d(st + p.a_bytes, tmB, k0, 0, b0, fb, polB);
+        if (PV) {
+            // column-pair boxes: an MN-major operand's K-chunk is KC / 2 pair
+            // rows; a K-major one's is two boxes of KC + 4 elements, the even
+            // columns (the first ld elements of the pair rows) and the odd
+            // ones (the next ld; box start rounded down to 16 bytes)
+            if (TA) {
+                tma_load_3d(st, tmA, k0, 0, b0, fb, polA);
+                tma_load_3d(st + (uint32_t)p.a_half, tmA, p.lda + k0 - (p.lda & 3), 0, b0, fb, polA);
+            } else {
+                tma_load_3d(st, tmA, 0, k0 >> 1, b0, fb, polA);
+            }
+            if (TB) {
+                tma_load_3d(st + p.a_bytes, tmB, 0, k0 >> 1, b0, fb, polB);
+            } else {
+                tma_load_3d(st + p.a_bytes, tmB, k0, 0, b0, fb, polB);
+                tma_load_3d(st + p.a_bytes + (uint32_t)p.b_half, tmB, p.ldb + k0 - (p.ldb & 3), 0, b0, fb, polB);
+            }
+        } else {
+            if (TA) tma_load_3d(st, tmA, k0, 0, b0, fb, polA);
+            else tma_load_3d(st, tmA, 0, k0, b0, fb, polA);
+            if (TB) tma_load_3d(st + p.a_bytes, tmB, 0, k0, b0, fb, polB);
+            else tma_load_3d(st + p.a_bytes, tmB, k0, 0, b0, fb, polB);
+        }
         if (++s == p.S) {
             s = 0;
             if (it >= 2 * p.S - 1) phase ^= 1u;
@@ -512,7 +574,7 @@ __device__ __forceinline__ void ksg_producer(const IaatKsgParams &p, const CUten
 #define IAAT_KSG_THREADS_OF(GW) (128 + 32 * (GW))
 #define IAAT_KSG_PRODUCER_REGS 40
 #define IAAT_KSG_CONSUMER_REGS_OF(GW) ((GW) == 8 ? 232 : 152)
-template <bool TA, bool TB, int MR, int NR, int LR, int KC, int KU, int G, int W, int DBG = 0>
+template <bool TA, bool TB, int MR, int NR, int LR, int KC, int KU, int G, int W, int DBG = 0, bool PV = false>
 __device__ __forceinline__ void ksg_body(const IaatKsgParams &p, const CUtensorMap *tmA, const CUtensorMap *tmB,
                                          const CUtensorMap *tmC)
 {
@@ -535,11 +597,11 @@ __device__ __forceinline__ void ksg_body(const IaatKsgParams &p, const CUtensorM
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp < 4) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(IAAT_KSG_PRODUCER_REGS));
-        if (warp < G) ksg_producer<TA, TB, KC, G, DBG>(p, tmA, tmB, tmC, smem, warp, lane);
+        if (warp < G) ksg_producer<TA, TB, KC, G, DBG, PV>(p, tmA, tmB, tmC, smem, warp, lane);
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(IAAT_KSG_CONSUMER_REGS_OF(G * W)));
         const int c = warp - 4;
-        ksg_consumer<TA, TB, MR, NR, LR, KC, KU, G, W, DBG>(p, smem, c / W, c % W, lane);
+        ksg_consumer<TA, TB, MR, NR, LR, KC, KU, G, W, DBG, PV>(p, smem, c / W, c % W, lane);
     }
 }
 

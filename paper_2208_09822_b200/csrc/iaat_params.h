@@ -154,6 +154,17 @@ struct IaatKsgParams {
     int beta_zero;
     int bm;                // warp blocks along Mv per problem
     int wpp;               // warp blocks per problem (bm * blocks along Nv)
+    // column-pair boxes (pairv = 1; kernel instances PV): packed operands
+    // whose ld's are even but not multiples of 4 (n = 2 mod 4: 8-byte, not
+    // 16-byte, column pitches) seen as tensors of column PAIRS -- rows of
+    // 2 * ld elements, a legal 16-byte TMA stride.  MN-major operands and C
+    // land exactly as before with pitch ld (= rows; 8-byte vector accesses);
+    // a K-major operand lands as two unswizzled boxes per K-chunk, even
+    // columns then odd columns (a_half / b_half bytes apart), rows of
+    // kc + 4 elements.  Rows past M of a warp block read the next column and
+    // are never stored.
+    int pairv;
+    int a_half, b_half;
     // slab staging (kernels iaat_ksgs_*): for inputs the TMA rules exclude
     // (ld's / strides / bases not 16-byte aligned).  Each stage holds the P
     // problems of a unit verbatim -- one cp.async.bulk per operand of the

@@ -456,21 +456,40 @@ bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
     const int64_t colsA = AK ? M : K, colsB = BK ? N : K, rowsA = AK ? K : M, rowsB = BK ? K : N;
     auto al16 = [&](int64_t el) { return (el * elt) % 16 == 0; };
     if (K < 1 || r.batch < 1 || r.batch >= ((int64_t)1 << 31)) return false;
-    // the TMA store of C writes whole 16-byte granules along M (measured:
-    // rows M .. round_up(M, 4) - 1 of an ld-padded C were overwritten), so C
-    // columns must end on a granule boundary
-    if (M % 4) return false;
-    // TMA boxes for A, B and C: 16-byte aligned bases, ld's and strides, no broadcast strides
-    if (r.align % 16 || !al16(r.lda) || !al16(r.ldb) || !al16(r.ldc)) return false;
+    // TMA boxes for A, B and C: 16-byte aligned bases and strides, no broadcast strides
+    if (r.align % 16) return false;
     if (r.batch > 1 && (!al16(r.sA) || !al16(r.sB) || !al16(r.sC) || r.sA < r.lda * colsA ||
                         r.sB < r.ldb * colsB || r.sC < r.ldc * N))
         return false;
+    // ... and 16-byte ld's.  The TMA store of C writes whole 16-byte granules
+    // along M (measured: rows M .. round_up(M, 4) - 1 of an ld-padded C were
+    // overwritten), so C columns must end on a granule boundary.
+    bool pv = false;
+    if (M % 4 || !al16(r.lda) || !al16(r.ldb) || !al16(r.ldc)) {
+        // Column-pair boxes (csrc/iaat_ksg.cuh PV, IaatKsgParams::pairv): even
+        // ld's that are not multiples of 4 (n = 2 mod 4) give 8-byte column
+        // pitches, which no TMA stride can express -- but TWO columns are a
+        // 16-byte multiple.  The operand is described as rows of 2 * ld
+        // elements (column pairs).  An MN-major operand (and C) must be packed
+        // (ld = rows, so that a pair row holds exactly two columns and the
+        // smem pitch stays uniform) with an even column count; a K-major one
+        // needs an even ld and an even column count (its dim 0 is ld + K:
+        // the odd column of the last pair ends where the problem ends).
+        auto pair_ok = [&](bool kmaj, int64_t rows, int64_t cols, int64_t ld) {
+            if (ld % 2 || cols % 2) return false;
+            return kmaj ? true : (ld == rows && 2 * ld <= 256);
+        };
+        if (std::getenv("IAAT_NO_PAIRV")) return false;
+        if (M % 2 || N % 2 || r.ldc != M || 2 * M > 256) return false;
+        if (!pair_ok(AK, rowsA, colsA, r.lda) || !pair_ok(BK, rowsB, colsB, r.ldb)) return false;
+        pv = true;
+    }
     const int64_t lim = (int64_t)1 << 40;
     if (r.sA * elt >= lim || r.sB * elt >= lim || r.sC * elt >= lim) return false;
     const int tidx = r.transA * 2 + r.transB;
     const int nent = (int)(sizeof(kKsgCatalog) / sizeof(kKsgCatalog[0]));
     struct Cand {
-        int idx = -1, Mv = 0, Nv = 0, P = 0, S = 0, cp = 0, bm = 0, wpp = 0, stage = 0, cbytes = 0;
+        int idx = -1, Mv = 0, Nv = 0, P = 0, S = 0, cp = 0, bm = 0, wpp = 0, stage = 0, cbytes = 0, a_reg = 0, b_reg = 0;
         double cost = 0;
     } best;
     const double bytes = (double)(M * K + K * N + M * N * (r.beta_zero ? 1 : 2)) * elt;
@@ -486,12 +505,21 @@ bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
         if (wpp > e.w || e.w % wpp) continue;
         const int P = e.w / wpp;
         int cp = Mv, bestwf = 1 << 30;
-        for (int pad = 0; pad < 32 && Mv + pad <= 256; pad += 4) {
+        for (int pad = 0; pad < 32 && Mv + pad <= 256 && !pv; pad += 4) {
             const int wf = ksg_epi_wavefronts(e, Mv + pad);
             if (wf < bestwf) bestwf = wf, cp = Mv + pad;
         }
-        const int a_tx = P * Mv * e.kc * elt, b_tx = P * Nv * e.kc * elt, c_tx = P * Nv * cp * elt;
-        const int stage = (int)(round_up(a_tx, 1024) + round_up(b_tx, 1024)), cbytes = (int)round_up(c_tx, 1024);
+        if (pv) cp = (int)M;  // the C buffer is the packed pair box: columns M apart
+        // pv: MN-major boxes hold the packed columns (pitch ld = rows), K-major
+        // ones two unswizzled half boxes of Mv / 2 (Nv / 2) rows of kc + 4
+        // elements (the odd columns' box starts ld % 4 elements early: TMA box
+        // starts are 16-byte aligned)
+        const int a_tx = pv ? P * (AK ? Mv * (e.kc + 4) : (int)r.lda * e.kc) * elt : P * Mv * e.kc * elt;
+        const int b_tx = pv ? P * (BK ? Nv * (e.kc + 4) : (int)r.ldb * e.kc) * elt : P * Nv * e.kc * elt;
+        const int c_tx = P * Nv * cp * elt;
+        const int a_reg = (int)(pv && AK ? 2 * round_up(a_tx / 2, 1024) : round_up(a_tx, 1024));
+        const int b_reg = (int)(pv && BK ? 2 * round_up(b_tx / 2, 1024) : round_up(b_tx, 1024));
+        const int stage = a_reg + b_reg, cbytes = (int)round_up(c_tx, 1024);
         int S = 0;
         while (S < IAAT_KSG_MAX_STAGES && IAAT_KSG_BAR_BYTES + 1024 + e.g * ((S + 1) * stage + cbytes) <= IAAT_SMEM_LIMIT)
             ++S;
@@ -518,6 +546,8 @@ bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
             best.wpp = wpp;
             best.stage = stage;
             best.cbytes = cbytes;
+            best.a_reg = a_reg;
+            best.b_reg = b_reg;
             best.cost = t;
         }
     }
@@ -535,13 +565,19 @@ bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
     k.P = best.P;
     k.S = best.S;
     k.nchunks = (int)((K + e.kc - 1) / e.kc);
-    k.a_pitch = best.Mv;
-    k.b_pitch = best.Nv;
+    k.a_pitch = pv && !AK ? (int)r.lda : best.Mv;
+    k.b_pitch = pv && !BK ? (int)r.ldb : best.Nv;
     k.c_pitch = best.cp;
-    k.a_tx = best.P * best.Mv * e.kc * elt;
-    k.b_tx = best.P * best.Nv * e.kc * elt;
-    k.a_bytes = (int)round_up(k.a_tx, 1024);
-    k.b_bytes = (int)round_up(k.b_tx, 1024);
+    k.a_tx = pv && AK ? best.P * best.Mv * (e.kc + 4) * elt : best.P * k.a_pitch * e.kc * elt;
+    k.b_tx = pv && BK ? best.P * best.Nv * (e.kc + 4) * elt : best.P * k.b_pitch * e.kc * elt;
+    k.a_bytes = best.a_reg;
+    k.b_bytes = best.b_reg;
+    k.pairv = pv ? 1 : 0;
+    k.a_half = pv && AK ? best.a_reg / 2 : 0;
+    k.b_half = pv && BK ? best.b_reg / 2 : 0;
+    k.lda = (int)r.lda;
+    k.ldb = (int)r.ldb;
+    k.ldc = (int)r.ldc;
     k.stage_bytes = best.stage;
     k.c_tx = best.P * best.Nv * best.cp * elt;
     k.c_bytes = best.cbytes;
@@ -562,9 +598,23 @@ bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
             g.box[0] = (uint32_t)D;
             g.box[1] = (uint32_t)e.kc;
         }
+        if (pv) {
+            // rows of column pairs; a K-major half box takes KC elements of
+            // the even (coordinate k0) or odd (ld + k0) columns of D / 2 pairs
+            g.dim[0] = (uint64_t)(kmaj ? ld + rows : 2 * ld);
+            g.dim[1] = (uint64_t)(cols / 2);
+            g.stride[0] = (uint64_t)(2 * ld * elt);
+            if (kmaj) {
+                g.box[0] = (uint32_t)(e.kc + 4);
+                g.box[1] = (uint32_t)(D / 2);
+            } else {
+                g.box[0] = (uint32_t)(2 * ld);
+                g.box[1] = (uint32_t)(e.kc / 2);
+            }
+        }
         g.box[2] = (uint32_t)best.P;
-        g.swizzle128 = kmaj && e.kc == 32 ? 1 : 0;
-        g.swizzle64 = kmaj && e.kc == 16 ? 1 : 0;
+        g.swizzle128 = kmaj && e.kc == 32 && !pv ? 1 : 0;
+        g.swizzle64 = kmaj && e.kc == 16 && !pv ? 1 : 0;
     };
     geo(pl.tmA, rowsA, colsA, r.lda, r.sA, AK, best.Mv);
     geo(pl.tmB, rowsB, colsB, r.ldb, r.sB, BK, best.Nv);
@@ -576,6 +626,13 @@ bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
     pl.tmC.box[0] = (uint32_t)best.cp;
     pl.tmC.box[1] = (uint32_t)best.Nv;
     pl.tmC.box[2] = (uint32_t)best.P;
+    if (pv) {
+        pl.tmC.dim[0] = (uint64_t)(2 * M);
+        pl.tmC.dim[1] = (uint64_t)(N / 2);
+        pl.tmC.stride[0] = (uint64_t)(2 * M * elt);
+        pl.tmC.box[0] = (uint32_t)(2 * M);
+        pl.tmC.box[1] = (uint32_t)(best.Nv / 2);
+    }
     pl.ksg = 1;
     pl.kg_entry = best.idx;
     pl.family = IAAT_FAM_KSG;
@@ -1692,9 +1749,9 @@ std::string plan_json(const PlanRequest &r, const Plan &p)
         add("\"family\": \"ksg\", \"entry\": %d, \"mr\": %d, \"nr\": %d, \"lane_rows\": %d, \"kc\": %d, "
             "\"ku\": %d, \"groups\": %d, \"warps_per_group\": %d, \"Mv\": %d, \"Nv\": %d, \"P\": %d, \"S\": %d, "
             "\"c_pitch\": %d, \"grid\": %d, \"block\": %d, \"smem\": %d, \"nunits\": %lld, \"est\": %.0f, "
-            "\"memops\": %lld, ",
+            "\"memops\": %lld, \"pairv\": %d, \"stage_bytes\": %d, \"c_bytes\": %d, ",
             p.kg_entry, e.mr, e.nr, e.lr, e.kc, e.ku, e.g, e.w, q.Mv, q.Nv, q.P, q.S, q.c_pitch, p.grid, p.block,
-            p.smem, (long long)q.nunits, p.est_total, (long long)p.memops);
+            p.smem, (long long)q.nunits, p.est_total, (long long)p.memops, q.pairv, q.stage_bytes, q.c_bytes);
         s += "\"classes\": []}";
         return s;
     }

@@ -85,6 +85,64 @@ def test_ksg_every_entry_parity_and_bitwise_vs_slab(tr):
     assert ran >= 2 * len(ents), ran
 
 
+PV_SHAPES = [(38, 38, 38), (42, 50, 46), (78, 78, 78), (66, 70, 62), (58, 34, 74), (40, 40, 38), (36, 38, 40),
+             (74, 46, 18), (50, 50, 50)]
+
+
+@pytest.mark.parametrize("tr", ["NN", "NT", "TT"])
+def test_ksg_column_pair_boxes_every_entry(tr):
+    """Column-pair TMA boxes (csrc/iaat_ksg.cuh PV; planner.cpp plan_ksg): packed
+    operands with even ld's that are not multiples of 4 (8-byte column
+    pitches).  Every catalog entry forced on such shapes -- ragged K chunks, a
+    ragged last unit, rows past M that alias the next column (predicated
+    stores), beta == 0 with a NaN-filled C -- against the oracle and bitwise
+    against the slab family (the whole packed C: every neighbour intact)."""
+    ents = [e for e in _entries() if e["trans"] == tr]
+    ran = 0
+    try:
+        for e in ents:
+            for i, (M, N, K) in enumerate(PV_SHAPES):
+                beta = 0.0 if i % 3 == 1 else 0.5
+                _force(family=7, order=e["index"])
+                c = Case(F32, tr[0], tr[1], M, N, K, 301, 37, 1.5, beta)
+                p = _plan(c, beta)
+                if p.get("family") != "ksg" or p.get("entry") != e["index"] or not p.get("pairv"):
+                    continue
+                A, B, C = c.views()
+                if beta == 0:
+                    C.fill_(float("nan"))
+                c.run()
+                torch.cuda.synchronize()
+                c.check(sample_ids(c.batch, 48, 24))
+                got = c.C.clone()
+                _force(family=0)
+                c2 = Case(F32, tr[0], tr[1], M, N, K, 301, 37, 1.5, beta)
+                if beta == 0:
+                    c2.views()[2].fill_(float("nan"))
+                c2.run()
+                torch.cuda.synchronize()
+                assert bits_equal(got, c2.C), (tr, e, M, N, K, beta)
+                ran += 1
+    finally:
+        _force()
+    assert ran >= 2 * len(ents), ran
+
+
+def test_ksg_column_pair_default_plan_full_batch():
+    """n = 2 mod 4 squares at the held-out sweep's batch (256 MiB of operands):
+    the default plan is a ksg column-pair plan; first / last / random problems
+    against the oracle."""
+    for n in (38, 58, 78):
+        for tr in ("NN", "NT", "TT"):
+            batch = (256 << 20) // (3 * n * n * 4)
+            c = Case(F32, tr[0], tr[1], n, n, n, batch, 11, 1.5, 0.5)
+            p = _plan(c, 0.5)
+            assert p["family"] == "ksg" and p["pairv"] == 1, p
+            c.run()
+            torch.cuda.synchronize()
+            c.check(sample_ids(c.batch, 128, 256))
+
+
 def test_ksg_padding_and_gaps_untouched():
     """ld > rows and gapped problem strides: the TMA store writes exactly
     the M x N elements of every problem (NaN sentinels in the gaps stay)."""

@@ -63,16 +63,26 @@ def check_ksg_plan(p, tr, M, N):
     br, bc = e["lr"] * e["mr"], (32 // e["lr"]) * e["nr"]
     assert p["Mv"] % br == 0 and p["Nv"] % bc == 0
     assert M <= p["Mv"] < M + br and N <= p["Nv"] < N + bc
-    assert M % 4 == 0
     wpp = (p["Mv"] // br) * (p["Nv"] // bc)
     assert wpp * p["P"] == e["w"]
     assert e["g"] * e["w"] in (8, 12) and p["block"] == 128 + 32 * e["g"] * e["w"]
-    assert 1 <= p["S"] <= 8 and p["c_pitch"] >= p["Mv"] and p["c_pitch"] % 4 == 0
-    assert p["smem"] <= 227 * 1024
-    # every group's ring (S stages of one A box and one B box) and C buffer fit
+    assert p["smem"] <= 227 * 1024 and 1 <= p["S"] <= 8
     r1k = lambda x: -(-x // 1024) * 1024  # noqa: E731
     P, kc = p["P"], e["kc"]
-    group = p["S"] * (r1k(P * p["Mv"] * kc * 4) + r1k(P * p["Nv"] * kc * 4)) + r1k(P * p["Nv"] * p["c_pitch"] * 4)
+    if p["pairv"]:
+        # column-pair boxes (n = 2 mod 4): packed even extents, C columns M
+        # apart; MN-major boxes hold the packed columns, K-major ones two
+        # unswizzled half boxes (even / odd columns) with rows of kc + 4
+        assert M % 2 == 0 and N % 2 == 0 and p["c_pitch"] == M
+        a = 2 * r1k(P * p["Mv"] // 2 * (kc + 4) * 4) if tr[0] == "T" else r1k(P * M * kc * 4)
+        b = 2 * r1k(P * p["Nv"] // 2 * (kc + 4) * 4) if tr[1] == "N" else r1k(P * N * kc * 4)
+        group = p["S"] * (a + b) + r1k(P * p["Nv"] * M * 4)
+        assert p["stage_bytes"] == a + b
+    else:
+        assert M % 4 == 0
+        assert p["c_pitch"] >= p["Mv"] and p["c_pitch"] % 4 == 0
+        # every group's ring (S stages of one A box and one B box) and C buffer fit
+        group = p["S"] * (r1k(P * p["Mv"] * kc * 4) + r1k(P * p["Nv"] * kc * 4)) + r1k(P * p["Nv"] * p["c_pitch"] * 4)
     assert p["smem"] >= 2048 + e["g"] * group, (p, group)
     assert p["grid"] <= 148
 
