@@ -115,8 +115,19 @@ struct Geo {
     static constexpr int PAIR = (!AK && VA >= 2) ? 1 : ((!BK && VB >= 2) ? 2 : 0);
     static constexpr int BR = LR * MR;  // warp block rows
     static constexpr int BC = LC * NR;  // warp block columns
+    // PV column map: the C buffer's columns are M = 2 (mod 4) words apart and
+    // cannot be padded, so neighbouring lanes must sit FOUR columns apart
+    // (4 M = 8 or 24 mod 32: a quarter-warp's 8-word row groups fall in
+    // disjoint banks; one column apart they overlap 2-4 ways).  A lane owns
+    // groups of 4 adjacent columns, 4 LC apart; the NR % 4 left-over columns
+    // sit after the groups, NR % 4 per lane.
+    static constexpr int NG = NR / 4 * 4, RB = NR % 4;
     __device__ static __forceinline__ int row(int ti, int r) { return AK ? ti + LR * r : VA * (ti + LR * (r / VA)) + r % VA; }
-    __device__ static __forceinline__ int col(int tj, int c) { return BK ? tj + LC * c : VB * (tj + LC * (c / VB)) + c % VB; }
+    __device__ static __forceinline__ int col(int tj, int c)
+    {
+        if (PV) return c < NG ? 4 * LC * (c / 4) + 4 * tj + c % 4 : LC * NG + RB * tj + (c - NG);
+        return BK ? tj + LC * c : VB * (tj + LC * (c / VB)) + c % VB;
+    }
 };
 
 // Swizzled K-major row base: 16-byte chunk q of smem row ra (KC*4 bytes,
@@ -218,6 +229,89 @@ struct Opnd {
     }
 };
 
+// PV: op(B)'s fragment loads under Geo's PV column map (col = 4 LC g + 4 tj + j
+// for the grouped columns, LC NG + RB tj + j' for the NR % 4 left-over ones).
+// K-major (two unswizzled half boxes, rows of KC + 4 elements): a grouped
+// column's parity is j's, so two bases (even / odd half) + immediates serve
+// them; the left-over columns keep one byte offset each.  MN-major (pitch ld,
+// 8-byte aligned columns): one base for the groups, one for the left-overs.
+template <bool KMAJ, int R, int V, int L, int KC>
+struct OpndPV {
+    static constexpr int NG = R / 4 * 4, RB = R % 4;
+    static constexpr uint32_t RP = (uint32_t)((KC + 4) * 4);  // K-major: bytes per smem row
+    uint32_t be[2];                 // K-major: even / odd half base of the lane's groups; MN-major: be[0] = groups, be[1] = left-overs
+    uint32_t brem[RB ? RB : 1];     // K-major: byte offset of each left-over column
+    uint32_t pitch;                 // MN-major: bytes per k-step
+    // x0: first column of the warp block (C0), t: the lane's tj, pl: problem, ext: Nv
+    __device__ __forceinline__ void setup(int x0, int t, int pl, int ext, int half, int ld, int kcpitch)
+    {
+        if (KMAJ) {
+            be[0] = (uint32_t)(pl * (ext >> 1) + (x0 >> 1) + 2 * t) * RP;
+            be[1] = be[0] + (uint32_t)(half + (ld & 3) * 4);
+#pragma unroll
+            for (int j = 0; j < RB; ++j) {
+                const int x = x0 + L * NG + RB * t + j;
+                brem[j] = (uint32_t)((x & 1) * (half + (ld & 3) * 4)) + (uint32_t)(pl * (ext >> 1) + (x >> 1)) * RP;
+            }
+        } else {
+            be[0] = (uint32_t)((pl * kcpitch + x0 + 4 * t) * 4);
+            be[1] = (uint32_t)((pl * kcpitch + x0 + L * NG + RB * t) * 4);
+        }
+    }
+    // byte address of column c at k-step 0 of the stage (K-major) / element c of k-step row a (MN-major)
+    __device__ __forceinline__ uint32_t kaddr(uint32_t stage, int c) const
+    {
+        return c < NG ? stage + be[c & 1] + (uint32_t)(2 * L * (c / 4) + ((c % 4) >> 1)) * RP : stage + brem[c < NG ? 0 : c - NG];
+    }
+    __device__ __forceinline__ uint32_t maddr(uint32_t a, int c) const
+    {
+        return c < NG ? a + be[0] + (uint32_t)((4 * L * (c / 4) + c % 4) * 4) : a + be[1] + (uint32_t)((c - NG) * 4);
+    }
+    template <int KU>
+    __device__ __forceinline__ void load(float (&f)[KU][R], uint32_t stage, int kb) const
+    {
+        if (KMAJ) {
+#pragma unroll
+            for (int c = 0; c < R; ++c) {
+                const uint32_t a = kaddr(stage, c) + (uint32_t)kb * 4u;
+                if (KU == 4) {
+                    lds64(a, f[0][c], f[KU > 1 ? 1 : 0][c]);
+                    lds64(a + 8, f[KU > 2 ? 2 : 0][c], f[KU > 3 ? 3 : 0][c]);
+                } else if (KU == 2) {
+                    lds64(a, f[0][c], f[KU > 1 ? 1 : 0][c]);
+                } else {
+                    f[0][c] = lds32(a);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < KU; ++kk) {
+                const uint32_t a = stage + (uint32_t)(kb + kk) * pitch;
+#pragma unroll
+                for (int c = 0; c < R; c += V) {
+                    if (V == 2) lds64(maddr(a, c), f[kk][c], f[kk][c + 1 < R ? c + 1 : c]);
+                    else f[kk][c] = lds32(maddr(a, c));
+                }
+            }
+        }
+    }
+    __device__ __forceinline__ void load1(float (&f)[R], uint32_t stage, int k) const
+    {
+#pragma unroll
+        for (int c = 0; c < R; ++c)
+            f[c] = KMAJ ? lds32(kaddr(stage, c) + (uint32_t)k * 4u) : lds32(maddr(stage + (uint32_t)k * pitch, c));
+    }
+};
+
+template <bool PV, typename A, typename B>
+struct SelOpnd {
+    typedef B type;
+};
+template <typename A, typename B>
+struct SelOpnd<true, A, B> {
+    typedef A type;
+};
+
 #ifndef IAAT_KSG_EVICT_FIRST
 #define IAAT_KSG_EVICT_FIRST 0
 #endif
@@ -306,7 +400,7 @@ __device__ __forceinline__ void ksg_consumer(const IaatKsgParams &p, unsigned ch
     const Smem sm(smem, p, g);
 
     Opnd<AK, MR, Gm::VA, LR, KC, PV> oa;
-    Opnd<BK, NR, Gm::VB, Gm::LC, KC, PV> ob;
+    typename SelOpnd<PV, OpndPV<BK, NR, Gm::VB, Gm::LC, KC>, Opnd<BK, NR, Gm::VB, Gm::LC, KC, false>>::type ob;
     // PV: byte offset of K-major row / column x of problem pl -- even ones in
     // the first half box, odd ones in the second, ld % 4 elements into the row
     auto pvrow = [&](int x, int ext, int half, int ld) {
@@ -320,9 +414,9 @@ __device__ __forceinline__ void ksg_consumer(const IaatKsgParams &p, unsigned ch
     } else {
         oa.base[0] = (uint32_t)((pl * KC * p.a_pitch + R0 + Gm::VA * ti) * 4);
     }
-    if (BK && PV) {
-        ob.base[0] = pvrow(C0 + Gm::col(tj, 0), Nv, p.b_half, p.ldb);
-    } else if (BK) {
+    if constexpr (PV) {
+        ob.setup(C0, tj, pl, Nv, p.b_half, p.ldb, KC * p.b_pitch);
+    } else if constexpr (BK) {
 #pragma unroll
         for (int c = 0; c < NR; ++c) ob.base[c] = kmaj_base<KC>(pl * Nv + C0 + Gm::col(tj, c));
     } else {
@@ -364,6 +458,9 @@ __device__ __forceinline__ void ksg_consumer(const IaatKsgParams &p, unsigned ch
                     kblock_fma<KU, MR, NR, Gm::PAIR>(acc, fa[cur], fb[cur]);
                 }
             } else {
+                // (ragged last chunk: software-pipelined pieces of 16 / 8 / 4
+                // k-steps instead of this loop measured neutral -- n = 76
+                // entry 0 95.2 us either way, r2s4_g7 -- the chunk is FMA-bound)
                 int kb = 0;
 #pragma unroll 1
                 for (; kb + 4 <= kv; kb += 4) {

@@ -517,9 +517,12 @@ bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
         const int a_tx = pv ? P * (AK ? Mv * (e.kc + 4) : (int)r.lda * e.kc) * elt : P * Mv * e.kc * elt;
         const int b_tx = pv ? P * (BK ? Nv * (e.kc + 4) : (int)r.ldb * e.kc) * elt : P * Nv * e.kc * elt;
         const int c_tx = P * Nv * cp * elt;
-        const int a_reg = (int)(pv && AK ? 2 * round_up(a_tx / 2, 1024) : round_up(a_tx, 1024));
-        const int b_reg = (int)(pv && BK ? 2 * round_up(b_tx / 2, 1024) : round_up(b_tx, 1024));
-        const int stage = a_reg + b_reg, cbytes = (int)round_up(c_tx, 1024);
+        // (pv boxes are all unswizzled: 128-byte alignment is enough, and the
+        // smaller regions buy ring depth -- n = 54: S = 1 -> 2)
+        const int ral = pv ? 128 : 1024;
+        const int a_reg = (int)(pv && AK ? 2 * round_up(a_tx / 2, ral) : round_up(a_tx, ral));
+        const int b_reg = (int)(pv && BK ? 2 * round_up(b_tx / 2, ral) : round_up(b_tx, ral));
+        const int stage = a_reg + b_reg, cbytes = (int)round_up(c_tx, ral);
         int S = 0;
         while (S < IAAT_KSG_MAX_STAGES && IAAT_KSG_BAR_BYTES + 1024 + e.g * ((S + 1) * stage + cbytes) <= IAAT_SMEM_LIMIT)
             ++S;

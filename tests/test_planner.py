@@ -74,9 +74,10 @@ def check_ksg_plan(p, tr, M, N):
         # apart; MN-major boxes hold the packed columns, K-major ones two
         # unswizzled half boxes (even / odd columns) with rows of kc + 4
         assert M % 2 == 0 and N % 2 == 0 and p["c_pitch"] == M
-        a = 2 * r1k(P * p["Mv"] // 2 * (kc + 4) * 4) if tr[0] == "T" else r1k(P * M * kc * 4)
-        b = 2 * r1k(P * p["Nv"] // 2 * (kc + 4) * 4) if tr[1] == "N" else r1k(P * N * kc * 4)
-        group = p["S"] * (a + b) + r1k(P * p["Nv"] * M * 4)
+        r128 = lambda x: -(-x // 128) * 128  # noqa: E731
+        a = 2 * r128(P * p["Mv"] // 2 * (kc + 4) * 4) if tr[0] == "T" else r128(P * M * kc * 4)
+        b = 2 * r128(P * p["Nv"] // 2 * (kc + 4) * 4) if tr[1] == "N" else r128(P * N * kc * 4)
+        group = p["S"] * (a + b) + r128(P * p["Nv"] * M * 4)
         assert p["stage_bytes"] == a + b
     else:
         assert M % 4 == 0
