@@ -170,6 +170,13 @@ def workload(cfg):
                 S.append(Shape("f64", tr, n, n, n, b, 1.5, 0.5, 1))
         desc = ("fp64 TN/TT (SURVEY f2; TN above 32^3 via iaat_set_tn_limit(80^3)): M=N=K in {8,...,80}, "
                 "batch=floor(256MiB/(3n^2*8B)), alpha=1.5, beta=0.5, seed 1")
+    elif cfg == 10:  # held-out sweep: n = 2 (mod 4), no tuning-table entries
+        for n in range(38, 80, 4):
+            b = (256 * 1024 * 1024) // (3 * n * n * 4)
+            for tr in ("NN", "NT", "TT"):
+                S.append(Shape("f32", tr, n, n, n, b, 1.5, 0.5, 1))
+        desc = ("held-out fp32 squares M=N=K in {38,42,...,78} x {NN,NT,TT} (8-byte column pitches: ksg column-pair TMA "
+                "boxes, cost-model plans only), batch=floor(256MiB/(3n^2*4B)), alpha=1.5, beta=0.5, seed 1")
     else:
         raise SystemExit("unknown config %r" % cfg)
     return S, desc
@@ -387,7 +394,7 @@ def run_ours(args, rank, world, local_rank):
             "dtype": shapes[0].dtype, "data": "synthetic",
             "config": {"workload": desc, "calls_per_step": len(chunks),
                        "l2": "inputs larger than L2: every call streams its own 256 MiB operand set "
-                             "(126 MB L2), no flush kernel needed" if args.config == 2 else
+                             "(126 MB L2), no flush kernel needed" if args.config in (2, 10) else
                              "as workload states", "parallelism": "dp%d (batch shards, no collective)" % world,
                        "timing": "K steps back to back, CUDA events at the two ends only; per-shape times "
                                  "and the roofline launch from a second pass with an event pair per call"},
@@ -800,7 +807,7 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2,
                     help="BASELINE.json configs 1-5; 6/7 = complex fp32/fp64 sweeps (SURVEY f1); "
-                         "8/9 = fp32 TN above 32^3, fp64 TN/TT (SURVEY f2)")
+                         "8/9 = fp32 TN above 32^3, fp64 TN/TT (SURVEY f2); 10 = held-out n = 2 (mod 4) squares")
     ap.add_argument("--cpu-frac", type=float, default=0.5)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")

@@ -475,9 +475,11 @@ bool plan_ksg(const PlanRequest &r, const Knobs &kn, Plan &out)
         // smem pitch stays uniform) with an even column count; a K-major one
         // needs an even ld and an even column count (its dim 0 is ld + K:
         // the odd column of the last pair ends where the problem ends).
+        // (a K-major operand with a padded even ld would work the same way; it
+        // is left to the slab family until a test covers it)
         auto pair_ok = [&](bool kmaj, int64_t rows, int64_t cols, int64_t ld) {
-            if (ld % 2 || cols % 2) return false;
-            return kmaj ? true : (ld == rows && 2 * ld <= 256);
+            if (ld % 2 || cols % 2 || ld != rows) return false;
+            return kmaj || 2 * ld <= 256;
         };
         if (std::getenv("IAAT_NO_PAIRV")) return false;
         if (M % 2 || N % 2 || r.ldc != M || 2 * M > 256) return false;

@@ -103,8 +103,9 @@ def test_ksg_column_pair_boxes_every_entry(tr):
         for e in ents:
             for i, (M, N, K) in enumerate(PV_SHAPES):
                 beta = 0.0 if i % 3 == 1 else 0.5
+                spad = 8 if i % 4 == 3 else 0  # gapped problem strides (16-byte multiples)
                 _force(family=7, order=e["index"])
-                c = Case(F32, tr[0], tr[1], M, N, K, 301, 37, 1.5, beta)
+                c = Case(F32, tr[0], tr[1], M, N, K, 301, 37, 1.5, beta, spad=spad)
                 p = _plan(c, beta)
                 if p.get("family") != "ksg" or p.get("entry") != e["index"] or not p.get("pairv"):
                     continue
@@ -116,7 +117,7 @@ def test_ksg_column_pair_boxes_every_entry(tr):
                 c.check(sample_ids(c.batch, 48, 24))
                 got = c.C.clone()
                 _force(family=0)
-                c2 = Case(F32, tr[0], tr[1], M, N, K, 301, 37, 1.5, beta)
+                c2 = Case(F32, tr[0], tr[1], M, N, K, 301, 37, 1.5, beta, spad=spad)
                 if beta == 0:
                     c2.views()[2].fill_(float("nan"))
                 c2.run()
