@@ -792,18 +792,26 @@ __device__ __forceinline__ void ksgs_consumer(const IaatKsgParams &p, unsigned c
     // element offsets (words) of the lane's rows / columns inside its problem
     // (the k-independent part): MN-major rows / columns are contiguous words,
     // K-major ones are ld apart
-    int oa[AK ? MR : 1], ob[BK ? NR : 1];
+    // ra / rb: byte address of each K-major row / column (of the first element
+    // of an MN-major operand) at k = 0 of the current unit -- the element
+    // offset here, the unit's stage address added before and taken off after
+    // the unit's k loop.  One register per K-major row: inside
+    // the unrolled k loop a load is [row + k * 4 + immediate], one add per
+    // row per four k-steps.  (The earlier form, (k-dependent base) + 4 *
+    // offset[r], cost one IMAD per row per k-step on the pipe the FFMA2s
+    // need: 10 of 41 instructions per k-step of the TN 8x4 tile.)
+    uint32_t ra[AK ? MR : 1], rb[BK ? NR : 1];
     if (AK) {
 #pragma unroll
-        for (int r = 0; r < MR; ++r) oa[r] = (R0 + Gm::row(ti, r)) * lda;
+        for (int r = 0; r < MR; ++r) ra[r] = (uint32_t)((R0 + Gm::row(ti, r)) * lda * 4);
     } else {
-        oa[0] = R0 + ti;
+        ra[0] = (uint32_t)((R0 + ti) * 4);
     }
     if (BK) {
 #pragma unroll
-        for (int c = 0; c < NR; ++c) ob[c] = (C0 + Gm::col(tj, c)) * ldb;
+        for (int c = 0; c < NR; ++c) rb[c] = (uint32_t)((C0 + Gm::col(tj, c)) * ldb * 4);
     } else {
-        ob[0] = C0 + tj;
+        rb[0] = (uint32_t)((C0 + tj) * 4);
     }
     const int64_t sA = p.sA, sB = p.sB, sC = p.sC;
 
@@ -827,14 +835,17 @@ __device__ __forceinline__ void ksgs_consumer(const IaatKsgParams &p, unsigned c
             const uint32_t pb = st + (uint32_t)p.a_bytes + misB + (uint32_t)(pl * sB * 4);
             // k-step stride (bytes) of the MN-major operands
             const uint32_t ka = AK ? 4u : (uint32_t)lda * 4u, kb = BK ? 4u : (uint32_t)ldb * 4u;
-            uint32_t xa = pa + (AK ? 0u : (uint32_t)oa[0] * 4u), xb = pb + (BK ? 0u : (uint32_t)ob[0] * 4u);
-            auto frag = [&](float (&a)[MR], float (&bv)[NR], uint32_t ya, uint32_t yb) {
+            // fold this unit's stage addresses into the row / column registers
 #pragma unroll
-                for (int r = 0; r < MR; ++r)
-                    a[r] = lds32(AK ? ya + (uint32_t)oa[r] * 4u : ya + (uint32_t)(LR * r * 4));
+            for (int r = 0; r < (AK ? MR : 1); ++r) ra[r] += pa;
 #pragma unroll
-                for (int c = 0; c < NR; ++c)
-                    bv[c] = lds32(BK ? yb + (uint32_t)ob[c] * 4u : yb + (uint32_t)(Gm::LC * c * 4));
+            for (int c = 0; c < (BK ? NR : 1); ++c) rb[c] += pb;
+            // fragments of k-step k (da = k * ka, db = k * kb)
+            auto frag = [&](float (&a)[MR], float (&bv)[NR], uint32_t da, uint32_t db) {
+#pragma unroll
+                for (int r = 0; r < MR; ++r) a[r] = lds32(AK ? ra[r] + da : ra[0] + da + (uint32_t)(LR * r * 4));
+#pragma unroll
+                for (int c = 0; c < NR; ++c) bv[c] = lds32(BK ? rb[c] + db : rb[0] + db + (uint32_t)(Gm::LC * c * 4));
             };
             // register double buffering (the paper's ping-pang):
             // k + 1's fragments load while k's FFMA2s issue -- for tiles of
@@ -842,28 +853,36 @@ __device__ __forceinline__ void ksgs_consumer(const IaatKsgParams &p, unsigned c
             // register cap; they keep the plain unrolled loop)
             if constexpr (MR * NR > 72) {
 #pragma unroll 4
-                for (int k = 0; k < K; ++k, xa += ka, xb += kb) {
+                for (int k = 0; k < K; ++k) {
                     float a[MR], bv[NR];
-                    frag(a, bv, xa, xb);
+                    frag(a, bv, (uint32_t)k * ka, (uint32_t)k * kb);
                     acc.rank1([&](int i) { return a[i]; }, [&](int j) { return bv[j]; });
                 }
             } else {
-            float a0[MR], b0[NR], a1[MR], b1[NR];
-            frag(a0, b0, xa, xb);
-            int k = 0;
+                float a0[MR], b0[NR], a1[MR], b1[NR];
+                frag(a0, b0, 0u, 0u);
+                int k = 0;
+                // both prefetches of an iteration stay below K; the last one
+                // or two k-steps follow the loop (no load past the operand)
 #pragma unroll 2
-            for (; k + 2 <= K; k += 2) {
-                frag(a1, b1, xa + ka, xb + kb);
-                acc.rank1([&](int i) { return a0[i]; }, [&](int j) { return b0[j]; });
-                // k + 2 (clamped to the last k-step: a valid address, loaded and unused)
-                const uint32_t st2 = k + 2 < K ? 2u : 1u;
-                xa += st2 * ka;
-                xb += st2 * kb;
-                frag(a0, b0, xa, xb);
-                acc.rank1([&](int i) { return a1[i]; }, [&](int j) { return b1[j]; });
+                for (; k + 2 < K; k += 2) {
+                    frag(a1, b1, (uint32_t)(k + 1) * ka, (uint32_t)(k + 1) * kb);
+                    acc.rank1([&](int i) { return a0[i]; }, [&](int j) { return b0[j]; });
+                    frag(a0, b0, (uint32_t)(k + 2) * ka, (uint32_t)(k + 2) * kb);
+                    acc.rank1([&](int i) { return a1[i]; }, [&](int j) { return b1[j]; });
+                }
+                if (k + 2 == K) {
+                    frag(a1, b1, (uint32_t)(k + 1) * ka, (uint32_t)(k + 1) * kb);
+                    acc.rank1([&](int i) { return a0[i]; }, [&](int j) { return b0[j]; });
+                    acc.rank1([&](int i) { return a1[i]; }, [&](int j) { return b1[j]; });
+                } else if (k < K) {
+                    acc.rank1([&](int i) { return a0[i]; }, [&](int j) { return b0[j]; });
+                }
             }
-            if (k < K) acc.rank1([&](int i) { return a0[i]; }, [&](int j) { return b0[j]; });
-            }
+#pragma unroll
+            for (int r = 0; r < (AK ? MR : 1); ++r) ra[r] -= pa;
+#pragma unroll
+            for (int c = 0; c < (BK ? NR : 1); ++c) rb[c] -= pb;
         }
         if (CS) {
             // fused epilogue in the stage's C span (C_in bulk-loaded with A

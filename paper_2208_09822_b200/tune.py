@@ -441,7 +441,7 @@ def main(argv=None):
             dtype, tr, M, N, K, batch, alpha, beta = sh
             key = key_line({"f32": 0, "f64": 1, "c32": 2, "c64": 3}[dtype], tr, M, N, K, beta == 0)
             if a.ksg:
-                if dtype != "f32" or min(M, N) < (13 if tr == "TN" else 24):
+                if dtype != "f32" or min(M, N) < (13 if tr == "TN" else 11):
                     continue
                 kw, p = tune_ksg(sh, line_to_knobs(existing[key]) if key in existing else {}, log)
             else:
