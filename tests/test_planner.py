@@ -334,3 +334,27 @@ def test_fp64_default_is_k_streamed_dmma(monkeypatch):
                 assert p["a_pitch"] % 16 == 4
             if tr[1] == "T":
                 assert p["b_pitch"] % 16 == 4
+
+
+def test_column_pair_eligibility():
+    """Column-pair TMA boxes (planner.cpp plan_ksg, pairv): only packed operands
+    with even extents whose ld's miss the 16-byte rule; everything else keeps
+    its family (regular ksg boxes when the ld's are 16-byte multiples)."""
+    for tr in ("NN", "NT", "TT"):
+        p = plan(0, tr, 38, 38, 38)
+        assert p["family"] == "ksg" and p["pairv"] == 1 and p["c_pitch"] == 38, p
+        check_ksg_plan(p, tr, 38, 38)
+        p = plan(0, tr, 40, 40, 40)
+        assert p["family"] == "ksg" and p["pairv"] == 0, p
+        # padded ld's (not packed), odd extents, 4-byte-aligned bases: not the pair view
+        for kw in ({"pad": 2}, {"align": 4}, {"align": 8}):
+            q = plan(0, tr, 38, 38, 38, **kw)
+            assert q["family"] != "ksg", (kw, q)
+        for (M, N, K) in ((37, 38, 38), (38, 37, 38), (39, 39, 39)):
+            q = plan(0, tr, M, N, K)
+            assert q["family"] != "ksg", (M, N, K, q)
+    # an odd K leaves an MN-major operand with an odd column count (NN: A, NT: A and B, TT: B)
+    assert plan(0, "NN", 38, 38, 37)["family"] != "ksg"
+    # M a 16-byte multiple but N = ldb-rows not (NT: B is N x K): pair view for all three operands
+    p = plan(0, "NT", 40, 38, 36)
+    assert p["family"] == "ksg" and p["pairv"] == 1 and p["c_pitch"] == 40, p
